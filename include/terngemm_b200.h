@@ -1,0 +1,170 @@
+/*
+ * terngemm_b200.h — C ABI of the B200-native sparse ternary GEMM
+ *                   Y = X W + b  (optionally PReLU), W in {-1, 0, +1}^{K x N}.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `terngemm` (/root/reference/pkg/src/terngemm).  Every entry point below names
+ * the reference function it replaces (file:line, relative to
+ * /root/reference/pkg/src/terngemm).  The reference is Python; the binding a
+ * maintainer would add is a ctypes stub (INTEGRATION.md shows it).
+ *
+ * Conventions
+ *   - All array pointers are DEVICE pointers (cudaMalloc / torch CUDA storage),
+ *     except `tg_sizes*` / `int64_t*` outputs documented as host.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Calls are stream-ordered and asynchronous unless documented otherwise.
+ *   - Index arrays are int32, exactly the reference layouts (tcsc.py:1-14,
+ *     variants.py:86-101, variants.py:251-263).  Dense matrices are row-major
+ *     with an explicit leading dimension (elements).
+ *   - Every function returns a tg_status; the message of the last failure on
+ *     the calling thread is available from tg_last_error().  Preconditions are
+ *     checked before any launch (dimension mismatches -> TG_ERR_PARAM, the
+ *     reference's ParameterError; inconsistent sparse structure ->
+ *     TG_ERR_CORRUPT, the reference's CorruptionError).
+ *   - There is no CPU fallback: without a usable sm_100a device every compute
+ *     entry point fails with TG_ERR_CUDA.
+ */
+#ifndef TERNGEMM_B200_H
+#define TERNGEMM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TG_ABI_VERSION 1
+
+typedef enum {
+  TG_OK = 0,
+  TG_ERR_PARAM = 1,       /* errors.py:4   ParameterError   */
+  TG_ERR_CORRUPT = 2,     /* errors.py:8   CorruptionError  */
+  TG_ERR_CUDA = 3,        /* CUDA runtime / launch failure   */
+  TG_ERR_UNSUPPORTED = 4, /* device is not sm_100            */
+  TG_ERR_OVERFLOW = 5     /* an index array would exceed int32 (tcsc.py:24 INDEX_DTYPE) */
+} tg_status;
+
+/* Format kinds for the two-phase builder. */
+#define TG_FMT_TCSC 0                /* tcsc.py:35 Tcsc                      */
+#define TG_FMT_BLOCKED 1             /* variants.py:86 BlockedTcsc           */
+#define TG_FMT_INTERLEAVED_BLOCKED 2 /* variants.py:251 InterleavedBlockedTcsc */
+
+/* Orders of the interleaved-blocked gather kernel. */
+#define TG_ORDER_INTERLEAVED_BLOCKED 0 /* kernels/scalar.py:397-485 */
+#define TG_ORDER_VECTORIZED_OPTIMAL 1  /* kernels/simd.py:282-420   */
+
+/* Device-side status words, written by kernels (optional, may be NULL). */
+typedef struct {
+  int32_t bad_input;           /* bit0: W entry outside {-1,0,1}; bit1: index out of range; bit2: non-finite X */
+  int32_t nonfinite_output;    /* 1 if any produced Y entry is inf/nan (dense.py:77 DenseMatrix check) */
+  uint64_t nonpositive_outputs;/* #(y <= 0) before PReLU: the reference's `mults` counter (simd.py:410-417) */
+  int32_t corrupt;             /* bit0: duplicate (row, col); bit1: cell in both sign arrays (tcsc.py:95-114) */
+  int32_t _pad;
+} tg_device_flags;
+
+/* Host-side sizes reported by the builder's count phase. */
+typedef struct {
+  int64_t nnz_pos;      /* len(row_index_pos)  (TCSC / blocked)              */
+  int64_t nnz_neg;      /* len(row_index_neg)  (TCSC / blocked)              */
+  int64_t n_indices;    /* len(all_indices)    (interleaved-blocked, incl. dummies) */
+  int64_t num_blocks;   /* ceil(K / B)                                         */
+  int64_t offsets_len;  /* elements of each offset table                        */
+} tg_sizes;
+
+/* ------------------------------------------------------------------ misc */
+int tg_abi_version(void);
+const char* tg_last_error(void);
+/* 1 if device `dev` is a compute-capability 10.0 (sm_100) GPU this library can run on. */
+int tg_device_supported(int dev);
+
+/* ------------------------------------------------------------------ format construction
+ * Two-phase device builder, bit-exact with the reference builders:
+ *   tcsc.py:71-92           tcsc_from_dense(W)
+ *   variants.py:146-178     blocked_from_dense(W, B)
+ *   variants.py:312-350     interleaved_blocked_from_dense(W, B, g, symmetric_cols)
+ * Phase 1 (tg_build_count) validates W (ParameterError for entries outside
+ * {-1,0,+1}, dense.py:45-49), counts every (block, column) cell and returns
+ * the output sizes; it synchronises `stream`.  Phase 2 (tg_build_fill_*)
+ * writes the arrays, stream-ordered.  `ws` must hold
+ * tg_build_workspace_bytes(K, N, B) bytes and stay untouched between phases.
+ * B is the resolved block size (variants.py:38-42); use B = K for TCSC.     */
+size_t tg_build_workspace_bytes(int64_t K, int64_t N, int64_t B);
+int tg_build_count(const int8_t* W, int64_t K, int64_t N, int64_t ldw, int kind, int64_t B, int g,
+                   int symmetric, void* ws, size_t ws_bytes, tg_sizes* sizes /* host */, void* stream);
+int tg_build_fill_tcsc(const void* ws, int64_t K, int64_t N, int32_t* col_start_pos, int32_t* row_index_pos,
+                       int32_t* col_start_neg, int32_t* row_index_neg, void* stream);
+int tg_build_fill_blocked(const void* ws, int64_t K, int64_t N, int64_t B, int32_t* col_start_pos /* nb x (N+1) */,
+                          int32_t* row_index_pos, int32_t* col_start_neg /* nb x (N+1) */, int32_t* row_index_neg,
+                          void* stream);
+int tg_build_fill_interleaved_blocked(const void* ws, int64_t K, int64_t N, int64_t B, int g, int symmetric,
+                                      int32_t* all_indices, int32_t* col_segment_ptr /* 3*nb*N+1 */,
+                                      void* stream);
+
+/* ------------------------------------------------------------------ ternary tiles
+ * GPU-native re-encoding of any of the formats above for the dense-decode
+ * tensor-core path: 2 bits per (k, n), grouped in 128-row x 1-column tiles.
+ * Built from the format's own device arrays (never from a host copy).
+ * Duplicate / overlapping entries set flags->corrupt (tcsc.py:105-113).        */
+size_t tg_tiles_bytes(int64_t K, int64_t N);
+int tg_tiles_from_dense(const int8_t* W, int64_t K, int64_t N, int64_t ldw, uint32_t* tiles,
+                        tg_device_flags* flags, void* stream);
+int tg_tiles_from_tcsc(const int32_t* col_start_pos, const int32_t* row_index_pos, const int32_t* col_start_neg,
+                       const int32_t* row_index_neg, int64_t K, int64_t N, uint32_t* tiles,
+                       tg_device_flags* flags, void* stream);
+int tg_tiles_from_blocked(const int32_t* col_start_pos, const int32_t* row_index_pos,
+                          const int32_t* col_start_neg, const int32_t* row_index_neg, int64_t K, int64_t N,
+                          int64_t B, uint32_t* tiles, tg_device_flags* flags, void* stream);
+int tg_tiles_from_interleaved_blocked(const int32_t* all_indices, const int32_t* col_segment_ptr, int64_t K,
+                                      int64_t N, int64_t B, int g, uint32_t* tiles, tg_device_flags* flags,
+                                      void* stream);
+/* Decode tiles back to dense int8 W (K x N, ld = N): tcsc.py:95 tcsc_to_dense. */
+int tg_tiles_to_dense(const uint32_t* tiles, int64_t K, int64_t N, int8_t* W, void* stream);
+
+/* ------------------------------------------------------------------ GEMM
+ * Workspace for any GEMM entry point below (X copies, limb split). */
+size_t tg_gemm_workspace_bytes(int64_t M, int64_t K, int64_t N);
+
+/* Gather path (CUDA cores, fp32 adds in the reference's own order, so the
+ * output is bit-identical to the reference kernel for any finite X):
+ *   gemm_base            kernels/scalar.py:109-148   (also `unrolled`, scalar.py:156-278)
+ *   gemm_blocked         kernels/scalar.py:286-389
+ *   gemm_interleaved_blocked / gemm_vectorized_optimal
+ *                        kernels/scalar.py:397-511, kernels/simd.py:282-449
+ * X is M x K (ldx >= K; an M x (K+1) PaddedInput, simd.py:40-75, passes ldx = K+1).
+ * use_alpha/alpha fuse the PReLU epilogue (simd.py:410-417).                     */
+/* uf = 0: gemm_base order (scalar.py:116-127); uf >= 1: gemm_unrolled's uf
+ * accumulator banks (scalar.py:167-206; uf = 1 equals the base order).     */
+int tg_gemm_tcsc(const float* X, int64_t M, int64_t K, int64_t ldx, const int32_t* col_start_pos,
+                 const int32_t* row_index_pos, const int32_t* col_start_neg, const int32_t* row_index_neg,
+                 int64_t N, const float* bias, float* Y, int64_t ldy, int uf, int use_alpha, float alpha, void* ws,
+                 size_t ws_bytes, tg_device_flags* flags, void* stream);
+/* uf, mr: gemm_blocked's banks for rows < floor(M/mr)*mr (scalar.py:296-358). */
+int tg_gemm_blocked(const float* X, int64_t M, int64_t K, int64_t ldx, int64_t B, const int32_t* col_start_pos,
+                    const int32_t* row_index_pos, const int32_t* col_start_neg, const int32_t* row_index_neg,
+                    int64_t N, const float* bias, float* Y, int64_t ldy, int uf, int mr, int use_alpha, float alpha,
+                    void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream);
+int tg_gemm_interleaved_blocked(const float* X, int64_t M, int64_t K, int64_t ldx, int64_t B, int g,
+                                const int32_t* all_indices, const int32_t* col_segment_ptr, int64_t N,
+                                const float* bias, float* Y, int64_t ldy, int order, int use_alpha, float alpha,
+                                void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream);
+
+/* Dense-decode tensor-core path (tcgen05.mma kind::i8 on exact int8 limbs of
+ * X, int32 accumulation in TMEM).  Same contract as the gather entry points;
+ * accumulation is exact, the only rounding is X's 22-23-bit per-row fixed
+ * point and one final fp64 -> fp32 rounding (bit-exact for integer X).
+ * Two launches: tg_gemm_tiles_prepare (X split) then tg_gemm_tiles_run; or
+ * tg_gemm_tiles for both.                                                     */
+int tg_gemm_tiles_prepare(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size_t ws_bytes,
+                          tg_device_flags* flags, void* stream);
+int tg_gemm_tiles_run(int64_t M, int64_t K, const uint32_t* tiles, int64_t N, const float* bias, float* Y,
+                      int64_t ldy, int use_alpha, float alpha, void* ws, size_t ws_bytes, tg_device_flags* flags,
+                      void* stream);
+int tg_gemm_tiles(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N,
+                  const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, void* ws, size_t ws_bytes,
+                  tg_device_flags* flags, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TERNGEMM_B200_H */

@@ -1,0 +1,226 @@
+// tg_capi.cu — extern "C" entry points declared in include/terngemm_b200.h.
+//
+// Argument checking lives here (before any launch); the kernels live in
+// tg_build.cu (format builders), tg_gather.cu (CUDA-core gather path) and
+// tg_mma.cu (dense-decode tensor-core path).
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "tg_internal.h"
+
+namespace tg {
+
+static thread_local std::string g_last_error;
+
+int set_error(int code, const char* msg) {
+  g_last_error = msg ? msg : "";
+  return code;
+}
+int set_cuda_error(cudaError_t e, const char* where) {
+  std::string m = std::string(where) + ": " + cudaGetErrorString(e);
+  g_last_error = m;
+  return TG_ERR_CUDA;
+}
+int check_launch(const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, where);
+  return TG_OK;
+}
+
+static int require_device() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaGetDevice");
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0)
+    return set_error(TG_ERR_UNSUPPORTED, "terngemm_b200 is built for sm_100a (B200) only");
+  return TG_OK;
+}
+
+#define TG_REQUIRE(cond, code, msg) \
+  do {                              \
+    if (!(cond)) return ::tg::set_error((code), (msg)); \
+  } while (0)
+#define TG_TRY(expr)         \
+  do {                       \
+    int _rc = (expr);        \
+    if (_rc != TG_OK) return _rc; \
+  } while (0)
+
+static inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+}  // namespace tg
+
+using namespace tg;
+
+extern "C" {
+
+int tg_abi_version(void) { return TG_ABI_VERSION; }
+
+const char* tg_last_error(void) { return g_last_error.c_str(); }
+
+int tg_device_supported(int dev) {
+  int major = 0, minor = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return (major == 10 && minor == 0) ? 1 : 0;
+}
+
+// ------------------------------------------------------------------ tiles
+size_t tg_tiles_bytes(int64_t K, int64_t N) {
+  if (K < 1 || N < 1) return 0;
+  return size_t(ceil_div(K, 128)) * size_t(round_up(N, 128)) * 8 * sizeof(uint32_t);
+}
+
+int tg_tiles_from_dense(const int8_t* W, int64_t K, int64_t N, int64_t ldw, uint32_t* tiles,
+                        tg_device_flags* flags, void* stream) {
+  TG_REQUIRE(K >= 1 && N >= 1, TG_ERR_PARAM, "K and N must be >= 1");
+  TG_REQUIRE(ldw >= N, TG_ERR_PARAM, "ldw must be >= N");
+  TG_REQUIRE(W && tiles, TG_ERR_PARAM, "null pointer");
+  TG_TRY(require_device());
+  return run_pack_dense(W, K, N, ldw, tiles, flags, as_stream(stream));
+}
+
+int tg_tiles_from_tcsc(const int32_t* csp, const int32_t* rip, const int32_t* csn, const int32_t* rin, int64_t K,
+                       int64_t N, uint32_t* tiles, tg_device_flags* flags, void* stream) {
+  TG_REQUIRE(K >= 1 && N >= 1, TG_ERR_PARAM, "K and N must be >= 1");
+  TG_REQUIRE(csp && csn && tiles, TG_ERR_PARAM, "null pointer");
+  TG_TRY(require_device());
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = cudaMemsetAsync(tiles, 0, tg_tiles_bytes(K, N), st);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaMemsetAsync(tiles)");
+  TG_TRY(run_pack_csc(csp, rip, N, 1, false, tiles, K, flags, st));
+  return run_pack_csc(csn, rin, N, 1, true, tiles, K, flags, st);
+}
+
+int tg_tiles_from_blocked(const int32_t* csp, const int32_t* rip, const int32_t* csn, const int32_t* rin,
+                          int64_t K, int64_t N, int64_t B, uint32_t* tiles, tg_device_flags* flags, void* stream) {
+  TG_REQUIRE(K >= 1 && N >= 1 && B >= 1, TG_ERR_PARAM, "K, N and B must be >= 1");
+  TG_REQUIRE(csp && csn && tiles, TG_ERR_PARAM, "null pointer");
+  TG_TRY(require_device());
+  cudaStream_t st = as_stream(stream);
+  const int64_t nb = ceil_div(K, B);
+  cudaError_t e = cudaMemsetAsync(tiles, 0, tg_tiles_bytes(K, N), st);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaMemsetAsync(tiles)");
+  TG_TRY(run_pack_csc(csp, rip, N, nb, false, tiles, K, flags, st));
+  return run_pack_csc(csn, rin, N, nb, true, tiles, K, flags, st);
+}
+
+int tg_tiles_from_interleaved_blocked(const int32_t* ai, const int32_t* ptr, int64_t K, int64_t N, int64_t B, int g,
+                                      uint32_t* tiles, tg_device_flags* flags, void* stream) {
+  TG_REQUIRE(K >= 1 && N >= 1 && B >= 1 && g >= 1, TG_ERR_PARAM, "K, N, B and g must be >= 1");
+  TG_REQUIRE(ptr && tiles, TG_ERR_PARAM, "null pointer");
+  TG_TRY(require_device());
+  cudaStream_t st = as_stream(stream);
+  const int64_t nb = ceil_div(K, B);
+  cudaError_t e = cudaMemsetAsync(tiles, 0, tg_tiles_bytes(K, N), st);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaMemsetAsync(tiles)");
+  return run_pack_ib(ai, ptr, N, nb, g, K, tiles, flags, st);
+}
+
+int tg_tiles_to_dense(const uint32_t* tiles, int64_t K, int64_t N, int8_t* W, void* stream) {
+  TG_REQUIRE(K >= 1 && N >= 1, TG_ERR_PARAM, "K and N must be >= 1");
+  TG_REQUIRE(tiles && W, TG_ERR_PARAM, "null pointer");
+  TG_TRY(require_device());
+  return run_unpack_dense(tiles, K, N, W, as_stream(stream));
+}
+
+// ------------------------------------------------------------------ GEMM (tiles)
+size_t tg_gemm_workspace_bytes(int64_t M, int64_t K, int64_t N) {
+  (void)N;
+  if (M < 1 || K < 1) return 0;
+  const size_t a = xsplit_bytes(M, K);
+  const size_t b = gather_ws_bytes(M, K);
+  return a > b ? a : b;
+}
+
+int tg_gemm_tiles_prepare(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size_t ws_bytes,
+                          tg_device_flags* flags, void* stream) {
+  TG_REQUIRE(M >= 1 && K >= 1, TG_ERR_PARAM, "M and K must be >= 1");
+  TG_REQUIRE(ldx >= K, TG_ERR_PARAM, "ldx must be >= K");
+  TG_REQUIRE(X && ws, TG_ERR_PARAM, "null pointer");
+  TG_REQUIRE(ws_bytes >= xsplit_bytes(M, K), TG_ERR_PARAM, "workspace too small");
+  TG_TRY(require_device());
+  return run_xsplit(X, M, K, ldx, ws, ws_bytes, flags, as_stream(stream));
+}
+
+int tg_gemm_tiles_run(int64_t M, int64_t K, const uint32_t* tiles, int64_t N, const float* bias, float* Y,
+                      int64_t ldy, int use_alpha, float alpha, void* ws, size_t ws_bytes, tg_device_flags* flags,
+                      void* stream) {
+  TG_REQUIRE(M >= 1 && K >= 1 && N >= 1, TG_ERR_PARAM, "M, K and N must be >= 1");
+  TG_REQUIRE(ldy >= N, TG_ERR_PARAM, "ldy must be >= N");
+  TG_REQUIRE(tiles && Y && ws, TG_ERR_PARAM, "null pointer");
+  TG_REQUIRE(ws_bytes >= xsplit_bytes(M, K), TG_ERR_PARAM, "workspace too small");
+  TG_REQUIRE(M <= (int64_t(1) << 30) && N <= (int64_t(1) << 30), TG_ERR_PARAM, "M, N too large");
+  TG_REQUIRE(K <= (int64_t(1) << 24), TG_ERR_PARAM, "K must be < 2^24 for exact int32 limb accumulation");
+  TG_TRY(require_device());
+  return run_mma(M, K, tiles, N, bias, Y, ldy, use_alpha, alpha, ws, flags, as_stream(stream));
+}
+
+int tg_gemm_tiles(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N,
+                  const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, void* ws, size_t ws_bytes,
+                  tg_device_flags* flags, void* stream) {
+  TG_TRY(tg_gemm_tiles_prepare(X, M, K, ldx, ws, ws_bytes, flags, stream));
+  return tg_gemm_tiles_run(M, K, tiles, N, bias, Y, ldy, use_alpha, alpha, ws, ws_bytes, flags, stream);
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ GEMM (gather)
+extern "C" {
+
+static int gather_common_checks(const float* X, int64_t M, int64_t K, int64_t ldx, int64_t N, float* Y, int64_t ldy,
+                                void* ws, size_t ws_bytes) {
+  TG_REQUIRE(M >= 1 && K >= 1 && N >= 1, TG_ERR_PARAM, "M, K and N must be >= 1");
+  TG_REQUIRE(ldx >= K && ldy >= N, TG_ERR_PARAM, "leading dimensions too small");
+  TG_REQUIRE(X && Y && ws, TG_ERR_PARAM, "null pointer");
+  TG_REQUIRE(ws_bytes >= gather_ws_bytes(M, K), TG_ERR_PARAM, "workspace too small");
+  TG_REQUIRE(K < (int64_t(1) << 31) - 1, TG_ERR_PARAM, "K too large for int32 indices");
+  return require_device();
+}
+
+int tg_gemm_tcsc(const float* X, int64_t M, int64_t K, int64_t ldx, const int32_t* csp, const int32_t* rip,
+                 const int32_t* csn, const int32_t* rin, int64_t N, const float* bias, float* Y, int64_t ldy, int uf,
+                 int use_alpha, float alpha, void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream) {
+  TG_TRY(gather_common_checks(X, M, K, ldx, N, Y, ldy, ws, ws_bytes));
+  TG_REQUIRE(csp && csn, TG_ERR_PARAM, "null offset table");
+  TG_REQUIRE(uf >= 0, TG_ERR_PARAM, "uf must be >= 0");
+  return run_gather(uf == 0 ? GATHER_BASE : GATHER_UNROLLED, X, M, K, ldx, csp, rip, csn, rin, 1, 1,
+                    uf == 0 ? 1 : uf, 0, N, bias, Y, ldy, use_alpha, alpha, ws, flags, as_stream(stream));
+}
+
+int tg_gemm_blocked(const float* X, int64_t M, int64_t K, int64_t ldx, int64_t B, const int32_t* csp,
+                    const int32_t* rip, const int32_t* csn, const int32_t* rin, int64_t N, const float* bias, float* Y,
+                    int64_t ldy, int uf, int mr, int use_alpha, float alpha, void* ws, size_t ws_bytes,
+                    tg_device_flags* flags, void* stream) {
+  TG_TRY(gather_common_checks(X, M, K, ldx, N, Y, ldy, ws, ws_bytes));
+  TG_REQUIRE(B >= 1, TG_ERR_PARAM, "block size must be >= 1");
+  TG_REQUIRE(uf >= 1 && mr >= 1, TG_ERR_PARAM, "uf and mr must be >= 1");
+  TG_REQUIRE(csp && csn, TG_ERR_PARAM, "null offset table");
+  const int64_t m_full = M / mr * mr;
+  return run_gather(GATHER_BLOCKED, X, M, K, ldx, csp, rip, csn, rin, ceil_div(K, B), 1, uf, m_full, N, bias, Y,
+                    ldy, use_alpha, alpha, ws, flags, as_stream(stream));
+}
+
+int tg_gemm_interleaved_blocked(const float* X, int64_t M, int64_t K, int64_t ldx, int64_t B, int g,
+                                const int32_t* ai, const int32_t* ptr, int64_t N, const float* bias, float* Y,
+                                int64_t ldy, int order, int use_alpha, float alpha, void* ws, size_t ws_bytes,
+                                tg_device_flags* flags, void* stream) {
+  TG_TRY(gather_common_checks(X, M, K, ldx, N, Y, ldy, ws, ws_bytes));
+  TG_REQUIRE(B >= 1 && g >= 1, TG_ERR_PARAM, "B and g must be >= 1");
+  TG_REQUIRE(ptr, TG_ERR_PARAM, "null col_segment_ptr");
+  TG_REQUIRE(order == TG_ORDER_INTERLEAVED_BLOCKED || order == TG_ORDER_VECTORIZED_OPTIMAL, TG_ERR_PARAM,
+             "unknown order");
+  return run_gather(order == TG_ORDER_INTERLEAVED_BLOCKED ? GATHER_IB : GATHER_OPTIMAL, X, M, K, ldx, ptr, ai,
+                    nullptr, nullptr, ceil_div(K, B), g, 1, 0, N, bias, Y, ldy, use_alpha, alpha, ws, flags,
+                    as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,240 @@
+// tg_gather.cu — CUDA-core gather-add path over the reference's own index
+// streams (no re-encoding).  Each output element Y[m, n] is accumulated by one
+// thread lane in exactly the reference kernel's fp32 operation order, so the
+// result is bit-identical to the reference for any finite input:
+//
+//   VAR_BASE      kernels/scalar.py:109-132  acc=0; acc+=x (pos); acc-=x (neg); out=b+acc
+//   VAR_UNROLLED  kernels/scalar.py:156-257  uf accumulator banks; bank u takes stream
+//                 positions start+u, start+u+uf, ...; the tail of each sign goes to
+//                 bank 0; tot = ((0 + bank0) + bank1) + ...; out = b + tot
+//   VAR_BLOCKED   kernels/scalar.py:286-367  out=b; per block: rows m < floor(M/mr)*mr use the
+//                 banked sum (out += tot), the leftover rows acc=0; +pos; -neg; out+=acc
+//   VAR_IB        kernels/scalar.py:397-485  out=b; per block: acc=0; runs of g (+,-); +rem; -rem; out+=acc
+//   VAR_OPTIMAL   kernels/simd.py:282-420    out=b; per block: acc over the interleaved segment
+//                 (sign = parity of t//g); out+=acc; out+=x (pos rem); out-=x (neg rem)
+//   then PReLU y = (y > 0) ? y : alpha*y in fp32 (simd.py:410-417).
+//
+// Layout: X is first transposed into Xt[K+1][M_pad] (row K = 0, the dummy slot
+// of PaddedInput, simd.py:40-75), so one warp-wide float4 load fetches X[m, k]
+// for 128 consecutive rows m: lanes = rows, one warp = one column n, the index
+// stream is read warp-uniformly (broadcast) from L1/L2.  Outputs are staged in
+// shared memory and written row-wise.
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "tg_internal.h"
+
+namespace tg {
+
+enum { VAR_BASE = 0, VAR_BLOCKED = 1, VAR_IB = 2, VAR_OPTIMAL = 3, VAR_UNROLLED = 4 };
+
+constexpr int G_WARPS = 8;    // columns per CTA
+constexpr int G_ROWS = 128;   // rows per CTA (4 per lane)
+
+size_t gather_ws_bytes(int64_t M, int64_t K) {
+  return size_t(K + 1) * size_t(round_up(M, G_ROWS)) * sizeof(float) + 256;
+}
+
+// X (M x ldx) -> Xt ((K+1) x M_pad), zero padded.
+__global__ void tg_transpose_kernel(const float* __restrict__ X, int64_t M, int64_t K, int64_t ldx,
+                                    float* __restrict__ Xt, int64_t M_pad, tg_device_flags* flags) {
+  __shared__ float tile[32][33];
+  const int64_t k0 = int64_t(blockIdx.x) * 32, m0 = int64_t(blockIdx.y) * 32;
+  bool bad = false;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t m = m0 + r, k = k0 + threadIdx.x;
+    float v = 0.f;
+    if (m < M && k < K) {
+      v = X[m * ldx + k];
+      bad |= !isfinite(v);
+    }
+    tile[r][threadIdx.x] = v;
+  }
+  if (flags && bad) atomicOr(&flags->bad_input, 4);
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t k = k0 + r, m = m0 + threadIdx.x;
+    if (k <= K && m < M_pad) Xt[k * M_pad + m] = tile[threadIdx.x][r];
+  }
+}
+
+__device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ void add4(float4& a, const float4 b) {
+  a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+}
+__device__ __forceinline__ void sub4(float4& a, const float4 b) {
+  a.x -= b.x; a.y -= b.y; a.z -= b.z; a.w -= b.w;
+}
+
+// Walk [a, b) of an index stream adding (NEG=false) or subtracting X rows into acc,
+// strictly in stream order.
+template <bool NEG>
+__device__ __forceinline__ void walk(float4& acc, const int32_t* __restrict__ idx, int32_t a, int32_t b,
+                                     const float* __restrict__ xt, int64_t ld) {
+  int32_t i = a;
+  for (; i + 4 <= b; i += 4) {
+    const int32_t k0 = __ldg(idx + i), k1 = __ldg(idx + i + 1), k2 = __ldg(idx + i + 2), k3 = __ldg(idx + i + 3);
+    const float4 v0 = ld4(xt + int64_t(k0) * ld), v1 = ld4(xt + int64_t(k1) * ld);
+    const float4 v2 = ld4(xt + int64_t(k2) * ld), v3 = ld4(xt + int64_t(k3) * ld);
+    if (NEG) { sub4(acc, v0); sub4(acc, v1); sub4(acc, v2); sub4(acc, v3); }
+    else { add4(acc, v0); add4(acc, v1); add4(acc, v2); add4(acc, v3); }
+  }
+  for (; i < b; ++i) {
+    const float4 v = ld4(xt + int64_t(__ldg(idx + i)) * ld);
+    if (NEG) sub4(acc, v); else add4(acc, v);
+  }
+}
+
+// Interleaved segment [s0, s1): alternating runs of g, positives first.
+__device__ __forceinline__ void walk_interleaved(float4& acc, const int32_t* __restrict__ ai, int32_t s0, int32_t s1,
+                                                 int g, const float* __restrict__ xt, int64_t ld) {
+  for (int32_t i = s0; i < s1; i += 2 * g) {
+    walk<false>(acc, ai, i, min(i + g, s1), xt, ld);
+    walk<true>(acc, ai, min(i + g, s1), min(i + 2 * g, s1), xt, ld);
+  }
+}
+
+// Banked sum of one (pos, neg) cell, kernels/scalar.py:167-206: every bank is an
+// independent sequential accumulation, so the banks are evaluated one after the
+// other and folded into tot in bank order -- two live accumulators for any uf.
+template <typename Acc>
+__device__ __forceinline__ Acc banked_sum(const int32_t* __restrict__ rp, int32_t ap, int32_t bp,
+                                          const int32_t* __restrict__ rn, int32_t an, int32_t bn, int uf,
+                                          const float* __restrict__ xt, int64_t ld) {
+  float4 tot = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int32_t fp = ap + (bp - ap) / uf * uf, fn = an + (bn - an) / uf * uf;
+  for (int u = 0; u < uf; ++u) {
+    float4 bank = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int32_t i = ap + u; i < fp; i += uf) add4(bank, ld4(xt + int64_t(__ldg(rp + i)) * ld));
+    if (u == 0) walk<false>(bank, rp, fp, bp, xt, ld);
+    for (int32_t i = an + u; i < fn; i += uf) sub4(bank, ld4(xt + int64_t(__ldg(rn + i)) * ld));
+    if (u == 0) walk<true>(bank, rn, fn, bn, xt, ld);
+    add4(tot, bank);
+  }
+  return tot;
+}
+
+template <int VAR>
+__global__ void __launch_bounds__(G_WARPS * 32)
+    tg_gather_kernel(const float* __restrict__ Xt, int64_t M_pad, int64_t M, int64_t N,
+                     const int32_t* __restrict__ p0, const int32_t* __restrict__ i0,   // pos (or all_indices/ptr)
+                     const int32_t* __restrict__ p1, const int32_t* __restrict__ i1,   // neg
+                     int64_t nblocks, int g, int uf, int64_t m_full, const float* __restrict__ bias,
+                     float* __restrict__ Y, int64_t ldy, int use_alpha, float alpha,
+                     tg_device_flags* __restrict__ flags) {
+  __shared__ float stage[G_ROWS][G_WARPS + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n = int64_t(blockIdx.x) * G_WARPS + warp;
+  const int64_t mrow = int64_t(blockIdx.y) * G_ROWS + lane * 4;
+  const float* xt = Xt + mrow;
+  float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (n < N) {
+    const float b = bias ? __ldg(bias + n) : 0.f;
+    if (VAR == VAR_BASE) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      walk<false>(acc, i0, __ldg(p0 + n), __ldg(p0 + n + 1), xt, M_pad);
+      walk<true>(acc, i1, __ldg(p1 + n), __ldg(p1 + n + 1), xt, M_pad);
+      out = make_float4(b + acc.x, b + acc.y, b + acc.z, b + acc.w);
+    } else if (VAR == VAR_UNROLLED) {
+      const float4 tot = banked_sum<float4>(i0, __ldg(p0 + n), __ldg(p0 + n + 1), i1, __ldg(p1 + n),
+                                            __ldg(p1 + n + 1), uf, xt, M_pad);
+      out = make_float4(b + tot.x, b + tot.y, b + tot.z, b + tot.w);
+    } else if (VAR == VAR_BLOCKED) {
+      // rows [0, m_full) take the banked order, rows [m_full, M) the plain one
+      const bool need_bank = mrow < m_full, need_plain = mrow + 4 > m_full;
+      out = make_float4(b, b, b, b);
+      for (int64_t blk = 0; blk < nblocks; ++blk) {
+        const int32_t* cp = p0 + blk * (N + 1);
+        const int32_t* cn = p1 + blk * (N + 1);
+        const int32_t ap = __ldg(cp + n), bp = __ldg(cp + n + 1), an = __ldg(cn + n), bn = __ldg(cn + n + 1);
+        float4 tot = make_float4(0.f, 0.f, 0.f, 0.f), acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (need_bank) tot = banked_sum<float4>(i0, ap, bp, i1, an, bn, uf, xt, M_pad);
+        if (need_plain) {
+          walk<false>(acc, i0, ap, bp, xt, M_pad);
+          walk<true>(acc, i1, an, bn, xt, M_pad);
+        }
+        out.x += (mrow + 0 < m_full) ? tot.x : acc.x;
+        out.y += (mrow + 1 < m_full) ? tot.y : acc.y;
+        out.z += (mrow + 2 < m_full) ? tot.z : acc.z;
+        out.w += (mrow + 3 < m_full) ? tot.w : acc.w;
+      }
+    } else {
+      // p0 = col_segment_ptr, i0 = all_indices
+      out = make_float4(b, b, b, b);
+      for (int64_t blk = 0; blk < nblocks; ++blk) {
+        const int64_t cell = blk * N + n;
+        const int32_t s0 = __ldg(p0 + 3 * cell), s1 = __ldg(p0 + 3 * cell + 1);
+        const int32_t s2 = __ldg(p0 + 3 * cell + 2), s3 = __ldg(p0 + 3 * cell + 3);
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        walk_interleaved(acc, i0, s0, s1, g, xt, M_pad);
+        if (VAR == VAR_IB) {
+          walk<false>(acc, i0, s1, s2, xt, M_pad);
+          walk<true>(acc, i0, s2, s3, xt, M_pad);
+          add4(out, acc);
+        } else {
+          add4(out, acc);
+          walk<false>(out, i0, s1, s2, xt, M_pad);
+          walk<true>(out, i0, s2, s3, xt, M_pad);
+        }
+      }
+    }
+  }
+  // epilogue: PReLU, flags, row-wise store through shared memory
+  float v[4] = {out.x, out.y, out.z, out.w};
+  bool bad = false;
+  unsigned long long npos = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const bool live = n < N && mrow + r < M;
+    if (use_alpha && !(v[r] > 0.f)) {
+      if (live) ++npos;
+      v[r] = alpha * v[r];
+    }
+    if (live) bad |= !isfinite(v[r]);
+    stage[lane * 4 + r][warp] = v[r];
+  }
+  if (flags) {
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&flags->nonfinite_output, 1);
+    for (int o = 16; o; o >>= 1) npos += __shfl_xor_sync(0xffffffffu, npos, o);
+    if (lane == 0 && npos) atomicAdd(reinterpret_cast<unsigned long long*>(&flags->nonpositive_outputs), npos);
+  }
+  __syncthreads();
+  const int64_t nbase = int64_t(blockIdx.x) * G_WARPS;
+  for (int e = threadIdx.x; e < G_ROWS * G_WARPS; e += blockDim.x) {
+    const int r = e / G_WARPS, c = e % G_WARPS;
+    const int64_t m = int64_t(blockIdx.y) * G_ROWS + r, nn = nbase + c;
+    if (m < M && nn < N) Y[m * ldy + nn] = stage[r][c];
+  }
+}
+
+int run_transpose(const float* X, int64_t M, int64_t K, int64_t ldx, float* Xt, int64_t M_pad,
+                  tg_device_flags* flags, cudaStream_t st) {
+  dim3 grid(unsigned(ceil_div(K + 1, 32)), unsigned(ceil_div(M_pad, 32)));
+  tg_transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(X, M, K, ldx, Xt, M_pad, flags);
+  return check_launch("tg_transpose_kernel");
+}
+
+int run_gather(int variant, const float* X, int64_t M, int64_t K, int64_t ldx, const int32_t* p0, const int32_t* i0,
+               const int32_t* p1, const int32_t* i1, int64_t nblocks, int g, int uf, int64_t m_full, int64_t N,
+               const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, void* ws,
+               tg_device_flags* flags, cudaStream_t st) {
+  const int64_t M_pad = round_up(M, G_ROWS);
+  float* Xt = static_cast<float*>(ws);
+  int rc = run_transpose(X, M, K, ldx, Xt, M_pad, flags, st);
+  if (rc != TG_OK) return rc;
+  dim3 grid(unsigned(ceil_div(N, G_WARPS)), unsigned(M_pad / G_ROWS));
+#define TG_GATHER_LAUNCH(V)                                                                         \
+  tg_gather_kernel<V><<<grid, G_WARPS * 32, 0, st>>>(Xt, M_pad, M, N, p0, i0, p1, i1, nblocks, g, uf, m_full, \
+                                                     bias, Y, ldy, use_alpha, alpha, flags)
+  switch (variant) {
+    case VAR_BASE: TG_GATHER_LAUNCH(VAR_BASE); break;
+    case VAR_UNROLLED: TG_GATHER_LAUNCH(VAR_UNROLLED); break;
+    case VAR_BLOCKED: TG_GATHER_LAUNCH(VAR_BLOCKED); break;
+    case VAR_IB: TG_GATHER_LAUNCH(VAR_IB); break;
+    default: TG_GATHER_LAUNCH(VAR_OPTIMAL); break;
+  }
+#undef TG_GATHER_LAUNCH
+  return check_launch("tg_gather_kernel");
+}
+
+}  // namespace tg

@@ -1,0 +1,43 @@
+// tg_internal.h — shared host-side helpers of the terngemm_b200 library.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstddef>
+#include <cstdint>
+#include <algorithm>
+
+#include "../../include/terngemm_b200.h"
+
+namespace tg {
+
+int set_error(int code, const char* msg);
+int set_cuda_error(cudaError_t e, const char* where);
+int check_launch(const char* where);
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
+
+// tg_mma.cu
+int mma_pick_mt(int64_t M);
+size_t xsplit_bytes(int64_t M, int64_t K);
+int run_xsplit(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size_t ws_bytes, tg_device_flags* flags,
+               cudaStream_t st);
+int run_mma(int64_t M, int64_t K, const uint32_t* tiles, int64_t N, const float* bias, float* Y, int64_t ldy,
+            int use_alpha, float alpha, void* ws, tg_device_flags* flags, cudaStream_t st);
+int run_pack_dense(const int8_t* W, int64_t K, int64_t N, int64_t ldw, uint32_t* tiles, tg_device_flags* flags,
+                   cudaStream_t st);
+int run_pack_csc(const int32_t* col_start, const int32_t* rows, int64_t N, int64_t nblocks, bool neg,
+                 uint32_t* tiles, int64_t K, tg_device_flags* flags, cudaStream_t st);
+int run_pack_ib(const int32_t* ai, const int32_t* ptr, int64_t N, int64_t nblocks, int g, int64_t K,
+                uint32_t* tiles, tg_device_flags* flags, cudaStream_t st);
+
+int run_unpack_dense(const uint32_t* tiles, int64_t K, int64_t N, int8_t* W, cudaStream_t st);
+
+// tg_gather.cu
+enum { GATHER_BASE = 0, GATHER_BLOCKED = 1, GATHER_IB = 2, GATHER_OPTIMAL = 3, GATHER_UNROLLED = 4 };
+size_t gather_ws_bytes(int64_t M, int64_t K);
+int run_gather(int variant, const float* X, int64_t M, int64_t K, int64_t ldx, const int32_t* p0, const int32_t* i0,
+               const int32_t* p1, const int32_t* i1, int64_t nblocks, int g, int uf, int64_t m_full, int64_t N,
+               const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, void* ws,
+               tg_device_flags* flags, cudaStream_t st);
+
+}  // namespace tg
