@@ -149,20 +149,51 @@ int tg_gemm_interleaved_blocked(const float* X, int64_t M, int64_t K, int64_t ld
                                 const float* bias, float* Y, int64_t ldy, int order, int use_alpha, float alpha,
                                 void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream);
 
-/* Dense-decode tensor-core path (tcgen05.mma kind::i8 on exact int8 limbs of
- * X, int32 accumulation in TMEM).  Same contract as the gather entry points;
- * accumulation is exact, the only rounding is X's 22-23-bit per-row fixed
- * point and one final fp64 -> fp32 rounding (bit-exact for integer X).
- * Two launches: tg_gemm_tiles_prepare (X split) then tg_gemm_tiles_run; or
- * tg_gemm_tiles for both.                                                     */
+/* Reference kernel whose fp32 operation order a gather walk reproduces. */
+#define TG_VARIANT_BASE 0               /* kernels/scalar.py:109-148 */
+#define TG_VARIANT_BLOCKED 1            /* kernels/scalar.py:286-389 */
+#define TG_VARIANT_INTERLEAVED_BLOCKED 2 /* kernels/scalar.py:397-511 */
+#define TG_VARIANT_VECTORIZED_OPTIMAL 3 /* kernels/simd.py:282-449  */
+#define TG_VARIANT_UNROLLED 4           /* kernels/scalar.py:156-278 */
+
+/* The format a tensor-core call was derived from, for the exact-order fix-up
+ * of rows the fixed-point limbs cannot carry (see tg_gemm_tiles).
+ *   BASE / UNROLLED: a0..a3 = col_start_pos, row_index_pos, col_start_neg, row_index_neg
+ *   BLOCKED:         same four arrays of the blocked format, plus B
+ *   INTERLEAVED_BLOCKED / VECTORIZED_OPTIMAL: a0 = col_segment_ptr, a1 = all_indices, B, g */
+typedef struct {
+  int32_t variant;
+  int32_t g;
+  int32_t uf;
+  int32_t mr;
+  int64_t B;
+  const int32_t* a0;
+  const int32_t* a1;
+  const int32_t* a2;
+  const int32_t* a3;
+} tg_format_ref;
+
+/* Dense-decode tensor-core path.
+ *   tg_gemm_tiles_prepare: every X row is scaled by a power of two so that
+ *     max|x| < 2^22, rounded, and split into three exact int8 limbs (one launch).
+ *   tg_gemm_tiles_run: tcgen05.mma.kind::i8 of the decoded ternary tiles against
+ *     the limbs with exact int32 accumulation in TMEM; the epilogue recombines the
+ *     limbs exactly, scales in fp64, adds the bias, rounds once to fp32 and
+ *     applies PReLU.  Rows whose nonzero entries span more than a 16x
+ *     max/rms dynamic range are then recomputed in the reference's exact order
+ *     from `exact` (a second, usually empty, launch); with exact == NULL they
+ *     keep the limb result.
+ * Bit-exact with the reference for integer-valued X; otherwise the only
+ * rounding is X's 22-bit per-row grid and one final rounding (~1e-7 normwise).
+ * tg_gemm_tiles = prepare + run.                                               */
 int tg_gemm_tiles_prepare(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size_t ws_bytes,
                           tg_device_flags* flags, void* stream);
-int tg_gemm_tiles_run(int64_t M, int64_t K, const uint32_t* tiles, int64_t N, const float* bias, float* Y,
-                      int64_t ldy, int use_alpha, float alpha, void* ws, size_t ws_bytes, tg_device_flags* flags,
-                      void* stream);
+int tg_gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N,
+                      const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, const tg_format_ref* exact,
+                      void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream);
 int tg_gemm_tiles(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N,
-                  const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, void* ws, size_t ws_bytes,
-                  tg_device_flags* flags, void* stream);
+                  const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, const tg_format_ref* exact,
+                  void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1,1 +1,56 @@
-"""B200-native sparse ternary GEMM (placeholder init)."""
+"""B200-native sparse ternary GEMM  Y = X W + b (+ fused PReLU).
+
+Drop-in for the hot path of the reference package ``terngemm``
+(/root/reference/pkg/src/terngemm/__init__.py): the same names for the data
+types, the three in-scope formats and their builders, the five in-scope
+GEMM variants and the variant registry — backed by hand-written sm_100a CUDA
+(csrc/) behind the C ABI in include/terngemm_b200.h.  There is no CPU path.
+"""
+
+from .dense import BiasVector, DenseMatrix, TernaryDense, oracle_gemm, prelu
+from .errors import CorruptionError, InvalidCodeError, ParameterError, ParseError, VerificationError
+from .formats import (
+    BlockedTcsc,
+    InterleavedBlockedTcsc,
+    Tcsc,
+    blocked_from_dense,
+    format_bytes,
+    interleaved_blocked_from_dense,
+    resolve_block_size,
+    tcsc_bytes_for,
+    tcsc_from_dense,
+    tcsc_to_dense,
+    validate,
+)
+from .harness import flop_count, operational_intensity
+from .kernels import (
+    DEFAULT_ALPHA,
+    SCALAR_TAGS,
+    SIMD_TAGS,
+    VARIANTS,
+    GemmConfig,
+    GemmRunner,
+    OpCount,
+    PaddedInput,
+    VariantSpec,
+    gemm_base,
+    gemm_blocked,
+    gemm_interleaved_blocked,
+    gemm_unrolled,
+    gemm_vectorized_optimal,
+    get_variant,
+    pad_input,
+    run_variant,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BiasVector", "BlockedTcsc", "CorruptionError", "DEFAULT_ALPHA", "DenseMatrix", "GemmConfig", "GemmRunner",
+    "InterleavedBlockedTcsc", "InvalidCodeError", "OpCount", "PaddedInput", "ParameterError", "ParseError",
+    "SCALAR_TAGS", "SIMD_TAGS", "Tcsc", "TernaryDense", "VARIANTS", "VariantSpec", "VerificationError",
+    "blocked_from_dense", "flop_count", "format_bytes", "gemm_base", "gemm_blocked", "gemm_interleaved_blocked",
+    "gemm_unrolled", "gemm_vectorized_optimal", "get_variant", "interleaved_blocked_from_dense",
+    "operational_intensity", "oracle_gemm", "pad_input", "prelu", "resolve_block_size", "run_variant",
+    "tcsc_bytes_for", "tcsc_from_dense", "tcsc_to_dense", "validate", "__version__",
+]

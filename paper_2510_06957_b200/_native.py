@@ -48,6 +48,27 @@ class TgSizes(ctypes.Structure):
     ]
 
 
+TG_VARIANT_BASE = 0
+TG_VARIANT_BLOCKED = 1
+TG_VARIANT_INTERLEAVED_BLOCKED = 2
+TG_VARIANT_VECTORIZED_OPTIMAL = 3
+TG_VARIANT_UNROLLED = 4
+
+
+class TgFormatRef(ctypes.Structure):
+    _fields_ = [
+        ("variant", ctypes.c_int32),
+        ("g", ctypes.c_int32),
+        ("uf", ctypes.c_int32),
+        ("mr", ctypes.c_int32),
+        ("B", ctypes.c_int64),
+        ("a0", ctypes.c_void_p),
+        ("a1", ctypes.c_void_p),
+        ("a2", ctypes.c_void_p),
+        ("a3", ctypes.c_void_p),
+    ]
+
+
 # tg_device_flags: int32 bad_input, int32 nonfinite_output, uint64 nonpositive_outputs,
 # int32 corrupt, int32 pad  -> 24 bytes; Python reads it back as 6 int32 words.
 FLAGS_BYTES = 24
@@ -85,8 +106,8 @@ SIGNATURES: dict[str, tuple] = {
         [_P, _I64, _I64, _I64, _I64, _I, _P, _P, _I64, _P, _P, _I64, _I, _I, _F, _P, _SZ, _P, _P],
     ),
     "tg_gemm_tiles_prepare": (_I, [_P, _I64, _I64, _I64, _P, _SZ, _P, _P]),
-    "tg_gemm_tiles_run": (_I, [_I64, _I64, _P, _I64, _P, _P, _I64, _I, _F, _P, _SZ, _P, _P]),
-    "tg_gemm_tiles": (_I, [_P, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _I, _F, _P, _SZ, _P, _P]),
+    "tg_gemm_tiles_run": (_I, [_P, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _I, _F, _P, _P, _SZ, _P, _P]),
+    "tg_gemm_tiles": (_I, [_P, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _I, _F, _P, _P, _SZ, _P, _P]),
 }
 
 _lock = threading.Lock()

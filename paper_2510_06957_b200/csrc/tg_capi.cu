@@ -151,24 +151,44 @@ int tg_gemm_tiles_prepare(const float* X, int64_t M, int64_t K, int64_t ldx, voi
   return run_xsplit(X, M, K, ldx, ws, ws_bytes, flags, as_stream(stream));
 }
 
-int tg_gemm_tiles_run(int64_t M, int64_t K, const uint32_t* tiles, int64_t N, const float* bias, float* Y,
-                      int64_t ldy, int use_alpha, float alpha, void* ws, size_t ws_bytes, tg_device_flags* flags,
-                      void* stream) {
+int tg_gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N,
+                      const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, const tg_format_ref* exact,
+                      void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream) {
   TG_REQUIRE(M >= 1 && K >= 1 && N >= 1, TG_ERR_PARAM, "M, K and N must be >= 1");
-  TG_REQUIRE(ldy >= N, TG_ERR_PARAM, "ldy must be >= N");
-  TG_REQUIRE(tiles && Y && ws, TG_ERR_PARAM, "null pointer");
+  TG_REQUIRE(ldy >= N && ldx >= K, TG_ERR_PARAM, "leading dimensions too small");
+  TG_REQUIRE(tiles && Y && ws && X, TG_ERR_PARAM, "null pointer");
   TG_REQUIRE(ws_bytes >= xsplit_bytes(M, K), TG_ERR_PARAM, "workspace too small");
   TG_REQUIRE(M <= (int64_t(1) << 30) && N <= (int64_t(1) << 30), TG_ERR_PARAM, "M, N too large");
   TG_REQUIRE(K <= (int64_t(1) << 24), TG_ERR_PARAM, "K must be < 2^24 for exact int32 limb accumulation");
+  if (exact) {
+    TG_REQUIRE(exact->variant >= 0 && exact->variant <= 4, TG_ERR_PARAM, "unknown exact variant");
+    TG_REQUIRE(exact->a0, TG_ERR_PARAM, "exact format without offsets");
+    TG_REQUIRE(exact->B >= 1 && exact->g >= 1 && exact->uf >= 1 && exact->mr >= 1, TG_ERR_PARAM,
+               "exact format: B, g, uf, mr must be >= 1");
+  }
   TG_TRY(require_device());
-  return run_mma(M, K, tiles, N, bias, Y, ldy, use_alpha, alpha, ws, flags, as_stream(stream));
+  cudaStream_t st = as_stream(stream);
+  TG_TRY(run_mma(M, K, tiles, N, bias, Y, ldy, use_alpha, alpha, ws, flags, st));
+  if (!exact) return TG_OK;
+  const int v = exact->variant;
+  const int64_t nb = (v == TG_VARIANT_BASE || v == TG_VARIANT_UNROLLED) ? 1 : ceil_div(K, exact->B);
+  const int64_t m_full = (v == TG_VARIANT_BLOCKED) ? M / exact->mr * exact->mr : 0;
+  const int uf = (v == TG_VARIANT_BASE) ? 1 : exact->uf;
+  if (v == TG_VARIANT_INTERLEAVED_BLOCKED || v == TG_VARIANT_VECTORIZED_OPTIMAL)
+    return run_fixup(v == TG_VARIANT_INTERLEAVED_BLOCKED ? GATHER_IB : GATHER_OPTIMAL, X, M, ldx,
+                     wide_rows(ws, M, K), exact->a0, exact->a1, nullptr, nullptr, nb, exact->g, 1, 0, N, bias, Y, ldy,
+                     use_alpha, alpha, flags, st);
+  const int gv = v == TG_VARIANT_BASE ? GATHER_BASE : v == TG_VARIANT_UNROLLED ? GATHER_UNROLLED : GATHER_BLOCKED;
+  return run_fixup(gv, X, M, ldx, wide_rows(ws, M, K), exact->a0, exact->a1, exact->a2, exact->a3, nb, 1, uf, m_full,
+                   N, bias, Y, ldy, use_alpha, alpha, flags, st);
 }
 
 int tg_gemm_tiles(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N,
-                  const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, void* ws, size_t ws_bytes,
-                  tg_device_flags* flags, void* stream) {
+                  const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, const tg_format_ref* exact,
+                  void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream) {
   TG_TRY(tg_gemm_tiles_prepare(X, M, K, ldx, ws, ws_bytes, flags, stream));
-  return tg_gemm_tiles_run(M, K, tiles, N, bias, Y, ldy, use_alpha, alpha, ws, ws_bytes, flags, stream);
+  return tg_gemm_tiles_run(X, M, K, ldx, tiles, N, bias, Y, ldy, use_alpha, alpha, exact, ws, ws_bytes, flags,
+                           stream);
 }
 
 }  // extern "C"

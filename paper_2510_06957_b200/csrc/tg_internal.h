@@ -19,6 +19,7 @@ inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
 // tg_mma.cu
 int mma_pick_mt(int64_t M);
 size_t xsplit_bytes(int64_t M, int64_t K);
+const int32_t* wide_rows(void* ws, int64_t M, int64_t K);
 int run_xsplit(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size_t ws_bytes, tg_device_flags* flags,
                cudaStream_t st);
 int run_mma(int64_t M, int64_t K, const uint32_t* tiles, int64_t N, const float* bias, float* Y, int64_t ldy,
@@ -39,5 +40,10 @@ int run_gather(int variant, const float* X, int64_t M, int64_t K, int64_t ldx, c
                const int32_t* p1, const int32_t* i1, int64_t nblocks, int g, int uf, int64_t m_full, int64_t N,
                const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, void* ws,
                tg_device_flags* flags, cudaStream_t st);
+
+int run_fixup(int variant, const float* X, int64_t M, int64_t ldx, const int32_t* rows, const int32_t* p0,
+              const int32_t* i0, const int32_t* p1, const int32_t* i1, int64_t nblocks, int g, int uf, int64_t m_full,
+              int64_t N, const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, tg_device_flags* flags,
+              cudaStream_t st);
 
 }  // namespace tg

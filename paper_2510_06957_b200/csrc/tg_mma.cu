@@ -33,14 +33,27 @@
 namespace tg {
 
 // ------------------------------------------------------------------ X split
-// One CTA per (padded) row.  limbs: [3][M_pad][K_pad] int8, rscale: [M_pad] f64.
+// One CTA per (padded) row.  limbs: [3][M_pad][K_pad] int8, rscale: [M_pad] f64,
+// wide: [1 + M_pad] int32 (count, then row ids).
+//
+// Row m is scaled by 2^s, s = 22 - e with amax < 2^e, so |x 2^s| < 2^22; the
+// rounded integer v splits into balanced base-256 digits v = d0 2^16 + d1 2^8 + d2.
+// The grid step 2^(e-22) is relative to the row maximum, so a row whose nonzero
+// entries span a wide dynamic range (amax > kWideRatio * rms of its nonzeros)
+// is listed in `wide` and later recomputed by the exact-order fix-up kernel;
+// its rscale is stored negated so the MMA epilogue leaves its PReLU count alone.
+constexpr float kWideRatio = 16.f;
+
 __global__ void __launch_bounds__(256) tg_xsplit_kernel(const float* __restrict__ X, int64_t M, int64_t K,
                                                         int64_t ldx, int8_t* __restrict__ limbs,
-                                                        double* __restrict__ rscale, int64_t M_pad,
-                                                        int64_t K_pad, tg_device_flags* __restrict__ flags) {
+                                                        double* __restrict__ rscale, int32_t* __restrict__ wide,
+                                                        int64_t M_pad, int64_t K_pad,
+                                                        tg_device_flags* __restrict__ flags) {
   const int64_t m = blockIdx.x;
   const float* row = X + m * ldx;
   __shared__ float red[8];
+  __shared__ float red2[8];
+  __shared__ int redn[8];
   float amax = 0.f;
   if (m < M) {
     for (int64_t k = threadIdx.x; k < K; k += blockDim.x) amax = fmaxf(amax, fabsf(row[k]));
@@ -51,9 +64,10 @@ __global__ void __launch_bounds__(256) tg_xsplit_kernel(const float* __restrict_
   amax = red[0];
 #pragma unroll
   for (int i = 1; i < 8; ++i) amax = fmaxf(amax, red[i]);
+  const bool finite = amax <= 3.402823466e38f;  // false for inf / nan
   int s = 0;
   if (m < M && amax > 0.f) {
-    if (!(amax <= 3.402823466e38f)) {  // inf or nan in the row
+    if (!finite) {
       if (threadIdx.x == 0 && flags) atomicOr(&flags->bad_input, 4);
     } else {
       int e;
@@ -61,17 +75,54 @@ __global__ void __launch_bounds__(256) tg_xsplit_kernel(const float* __restrict_
       s = 22 - e;        // |x * 2^s| < 2^22
     }
   }
-  if (threadIdx.x == 0) rscale[m] = (m < M && amax > 0.f) ? ldexp(1.0, -s) : 0.0;
+  // dynamic range of the nonzero entries: sum (x / amax)^2 and their count
+  bool is_wide = false;
+  if (m < M && amax > 0.f && finite) {
+    const float inv = 1.f / amax;
+    float s2 = 0.f;
+    int nz = 0;
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
+      const float t = row[k] * inv;
+      s2 += t * t;
+      nz += t != 0.f;
+    }
+    for (int o = 16; o; o >>= 1) {
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      nz += __shfl_xor_sync(0xffffffffu, nz, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      red2[threadIdx.x >> 5] = s2;
+      redn[threadIdx.x >> 5] = nz;
+    }
+    __syncthreads();
+    s2 = 0.f;
+    nz = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      s2 += red2[i];
+      nz += redn[i];
+    }
+    is_wide = float(nz) > kWideRatio * kWideRatio * s2;  // amax / rms(nonzeros) > kWideRatio
+  }
+  if (threadIdx.x == 0) {
+    const double sc = (m < M && amax > 0.f && finite) ? ldexp(1.0, -s) : 0.0;
+    rscale[m] = is_wide ? -sc : sc;
+    if (is_wide && wide) {
+      const int slot = atomicAdd(wide, 1);
+      wide[1 + slot] = int32_t(m);
+    }
+  }
   int8_t* l0 = limbs + m * K_pad;
   int8_t* l1 = limbs + (M_pad + m) * K_pad;
   int8_t* l2 = limbs + (2 * M_pad + m) * K_pad;
+  const bool live = m < M && amax > 0.f && finite;
   for (int64_t k0 = int64_t(threadIdx.x) * 4; k0 < K_pad; k0 += int64_t(blockDim.x) * 4) {
     uint32_t p0 = 0, p1 = 0, p2 = 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int64_t k = k0 + j;
       int v = 0;
-      if (m < M && k < K && amax > 0.f) v = __float2int_rn(ldexpf(row[k], s));
+      if (live && k < K) v = __float2int_rn(ldexpf(row[k], s));
       const int d2 = ((v + 128) & 255) - 128;
       const int v1 = (v - d2) >> 8;
       const int d1 = ((v1 + 128) & 255) - 128;
@@ -244,11 +295,12 @@ __global__ void __launch_bounds__(192, 1)
           const long long tot = (static_cast<long long>(static_cast<int>(r0[j])) << 16) +
                                 (static_cast<long long>(static_cast<int>(r1[j])) << 8) +
                                 static_cast<long long>(static_cast<int>(r2[j]));
-          const double v = static_cast<double>(tot) * __ldg(rscale + m) + bn;
+          const double rs = __ldg(rscale + m);  // < 0: wide row, the fix-up kernel owns its count
+          const double v = static_cast<double>(tot) * fabs(rs) + bn;
           float y = static_cast<float>(v);
           if (use_alpha && !(y > 0.f)) {
             y = alpha * y;
-            ++npos;
+            npos += rs >= 0.0;
           }
           any_bad |= !isfinite(y);
           Y[int64_t(m) * ldy + n] = y;
@@ -400,34 +452,50 @@ int mma_pick_mt(int64_t M) {
   return 64;
 }
 
-size_t xsplit_bytes(int64_t M, int64_t K) {
-  const int64_t mt = mma_pick_mt(M);
-  const int64_t M_pad = round_up(M, mt);
-  const int64_t K_pad = round_up(K, 128);
-  return size_t(3 * M_pad * K_pad) + size_t(M_pad) * sizeof(double) + 256;
+struct SplitLayout {
+  int64_t mt, M_pad, K_pad;
+  size_t off_rscale, off_wide, total;
+};
+
+static SplitLayout split_layout(int64_t M, int64_t K) {
+  SplitLayout L;
+  L.mt = mma_pick_mt(M);
+  L.M_pad = round_up(M, L.mt);
+  L.K_pad = round_up(K, 128);
+  L.off_rscale = size_t(round_up(3 * L.M_pad * L.K_pad, 256));
+  L.off_wide = L.off_rscale + size_t(round_up(L.M_pad * int64_t(sizeof(double)), 256));
+  L.total = L.off_wide + size_t(round_up((L.M_pad + 1) * 4, 256));
+  return L;
+}
+
+size_t xsplit_bytes(int64_t M, int64_t K) { return split_layout(M, K).total; }
+
+const int32_t* wide_rows(void* ws, int64_t M, int64_t K) {
+  return reinterpret_cast<const int32_t*>(static_cast<uint8_t*>(ws) + split_layout(M, K).off_wide);
 }
 
 int run_xsplit(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size_t ws_bytes, tg_device_flags* flags,
                cudaStream_t st) {
-  if (ws_bytes < xsplit_bytes(M, K)) return set_error(TG_ERR_PARAM, "workspace too small for X split");
-  const int64_t mt = mma_pick_mt(M);
-  const int64_t M_pad = round_up(M, mt);
-  const int64_t K_pad = round_up(K, 128);
-  int8_t* limbs = static_cast<int8_t*>(ws);
-  double* rscale = reinterpret_cast<double*>(static_cast<uint8_t*>(ws) + round_up(3 * M_pad * K_pad, 256));
-  tg_xsplit_kernel<<<unsigned(M_pad), 256, 0, st>>>(X, M, K, ldx, limbs, rscale, M_pad, K_pad, flags);
+  const SplitLayout L = split_layout(M, K);
+  if (ws_bytes < L.total) return set_error(TG_ERR_PARAM, "workspace too small for X split");
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  int8_t* limbs = reinterpret_cast<int8_t*>(base);
+  double* rscale = reinterpret_cast<double*>(base + L.off_rscale);
+  int32_t* wide = reinterpret_cast<int32_t*>(base + L.off_wide);
+  cudaError_t e = cudaMemsetAsync(wide, 0, sizeof(int32_t), st);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaMemsetAsync(wide rows)");
+  tg_xsplit_kernel<<<unsigned(L.M_pad), 256, 0, st>>>(X, M, K, ldx, limbs, rscale, wide, L.M_pad, L.K_pad, flags);
   return check_launch("tg_xsplit_kernel");
 }
 
 int run_mma(int64_t M, int64_t K, const uint32_t* tiles, int64_t N, const float* bias, float* Y, int64_t ldy,
             int use_alpha, float alpha, void* ws, tg_device_flags* flags, cudaStream_t st) {
-  const int64_t mt = mma_pick_mt(M);
-  const int64_t M_pad = round_up(M, mt);
-  const int64_t K_pad = round_up(K, 128);
+  const SplitLayout L = split_layout(M, K);
+  const int64_t mt = L.mt, M_pad = L.M_pad, K_pad = L.K_pad;
   const int64_t N_pad = round_up(N, 128);
   const int64_t KC = K_pad / 128;
   int8_t* limbs = static_cast<int8_t*>(ws);
-  double* rscale = reinterpret_cast<double*>(static_cast<uint8_t*>(ws) + round_up(3 * M_pad * K_pad, 256));
+  double* rscale = reinterpret_cast<double*>(static_cast<uint8_t*>(ws) + L.off_rscale);
 
   auto enc = get_encode();
   if (!enc) return set_error(TG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");

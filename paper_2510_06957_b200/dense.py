@@ -1,0 +1,250 @@
+"""Dense operand types of the drop-in API (reference: dense.py:32-111).
+
+Each type wraps either a host numpy array (validated on construction exactly
+like the reference) or a CUDA tensor (kept resident in HBM).  ``.values``
+always returns a host numpy array — the reference's contract — copying from
+the device lazily and once; ``.device_values`` returns the CUDA tensor,
+uploading lazily and once.  Kernel outputs are device-resident DenseMatrix
+objects whose finiteness check (dense.py:77) is carried by a device flag
+written by the kernel epilogue and raised on first host access, so the hot
+path never synchronises.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .errors import ParameterError
+
+EXACT_FLOAT32_BOUND = 2**24  # dense.py:17
+
+
+def _device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2510_06957_b200 needs a CUDA (sm_100a) device; there is no CPU path")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _is_tensor(v) -> bool:
+    return isinstance(v, torch.Tensor)
+
+
+class _Dual:
+    """Host/device pair with lazy, cached transfers."""
+
+    __slots__ = ("_h", "_d")
+
+    def __init__(self, host: np.ndarray | None, dev: torch.Tensor | None):
+        self._h = host
+        self._d = dev
+
+    def host(self) -> np.ndarray:
+        if self._h is None:
+            self._h = self._d.detach().cpu().numpy()
+        return self._h
+
+    def dev(self) -> torch.Tensor:
+        if self._d is None or not self._d.is_cuda:
+            self._d = torch.from_numpy(np.ascontiguousarray(self._h)).to(_device(), non_blocking=False)
+        return self._d
+
+    def shape(self):
+        return tuple(self._h.shape) if self._h is not None else tuple(self._d.shape)
+
+
+class TernaryDense:
+    """K x N weight matrix with entries in {-1, 0, +1} (dense.py:32-64).
+
+    Host input is validated here (ParameterError naming the first bad entry);
+    a CUDA tensor is validated by the device builder on first use."""
+
+    def __init__(self, values):
+        if _is_tensor(values):
+            v = values.detach()
+            if v.dtype != torch.int8:
+                v = v.to(torch.int8)
+            if v.dim() != 2 or v.shape[0] < 1 or v.shape[1] < 1:
+                raise ParameterError(f"ternary matrix must be 2-D and non-empty, got shape {tuple(values.shape)}")
+            self._v = _Dual(None, v.contiguous())
+            return
+        v = np.ascontiguousarray(values, dtype=np.int8)
+        raw = np.asarray(values)
+        if v.ndim != 2 or v.shape[0] < 1 or v.shape[1] < 1:
+            raise ParameterError(f"ternary matrix must be 2-D and non-empty, got shape {raw.shape}")
+        bad = (raw < -1) | (raw > 1) if raw.dtype.kind in "iuf" else (v < -1) | (v > 1)
+        if bad.any():
+            k, n = np.argwhere(bad)[0]
+            raise ParameterError(f"entry ({k}, {n}) = {raw[k, n]} is not in {{-1, 0, +1}}")
+        self._v = _Dual(v, None)
+
+    @property
+    def values(self) -> np.ndarray:
+        return self._v.host()
+
+    @property
+    def device_values(self) -> torch.Tensor:
+        return self._v.dev()
+
+    @property
+    def K(self) -> int:
+        return self._v.shape()[0]
+
+    @property
+    def N(self) -> int:
+        return self._v.shape()[1]
+
+    @property
+    def nnz(self) -> int:
+        if self._v._h is not None:
+            return int(np.count_nonzero(self._v._h))
+        return int(torch.count_nonzero(self._v._d).item())
+
+    def __eq__(self, other) -> bool:
+        return isinstance(other, TernaryDense) and np.array_equal(self.values, other.values)
+
+    def __repr__(self) -> str:
+        return f"TernaryDense(K={self.K}, N={self.N})"
+
+
+class DenseMatrix:
+    """Row-major float32 matrix with all entries finite (dense.py:67-90).
+
+    ``flags`` (internal) is the kernel-written device status word of an output;
+    its non-finite bit is turned into the reference's ParameterError the first
+    time the host looks at the values (or on ``check()``)."""
+
+    def __init__(self, values, _flags: torch.Tensor | None = None):
+        self._flags = _flags
+        self._checked = _flags is None
+        if _is_tensor(values):
+            v = values.detach()
+            if v.dim() != 2:
+                raise ParameterError(f"dense matrix must be 2-D, got shape {tuple(values.shape)}")
+            if v.dtype != torch.float32:
+                v = v.float()
+            self._v = _Dual(None, v.contiguous())
+            if _flags is None:
+                self._checked = False  # lazily checked with torch.isfinite
+            return
+        v = np.ascontiguousarray(values, dtype=np.float32)
+        if v.ndim != 2:
+            raise ParameterError(f"dense matrix must be 2-D, got shape {np.asarray(values).shape}")
+        if not np.isfinite(v).all():
+            raise ParameterError("dense matrix contains non-finite values")
+        self._v = _Dual(v, None)
+        self._checked = True
+
+    def check(self) -> "DenseMatrix":
+        if not self._checked:
+            if self._flags is not None:
+                bad = int(self._flags[1].item()) != 0
+            else:
+                bad = not bool(torch.isfinite(self._v._d).all().item())
+            if bad:
+                raise ParameterError("dense matrix contains non-finite values")
+            self._checked = True
+        return self
+
+    @property
+    def values(self) -> np.ndarray:
+        self.check()
+        return self._v.host()
+
+    @property
+    def device_values(self) -> torch.Tensor:
+        return self._v.dev()
+
+    @property
+    def rows(self) -> int:
+        return self._v.shape()[0]
+
+    @property
+    def cols(self) -> int:
+        return self._v.shape()[1]
+
+    def __eq__(self, other) -> bool:
+        return isinstance(other, DenseMatrix) and np.array_equal(self.values, other.values)
+
+    def __repr__(self) -> str:
+        return f"DenseMatrix({self.rows}x{self.cols})"
+
+
+class BiasVector:
+    """Length-N float32 vector broadcast over the output rows (dense.py:93-111)."""
+
+    def __init__(self, values):
+        if _is_tensor(values):
+            v = values.detach()
+            if v.dim() != 1:
+                raise ParameterError(f"bias must be 1-D, got shape {tuple(values.shape)}")
+            if v.dtype != torch.float32:
+                v = v.float()
+            if not bool(torch.isfinite(v).all().item()):
+                raise ParameterError("bias contains non-finite values")
+            self._v = _Dual(None, v.contiguous())
+            return
+        v = np.ascontiguousarray(values, dtype=np.float32)
+        if v.ndim != 1:
+            raise ParameterError(f"bias must be 1-D, got shape {np.asarray(values).shape}")
+        if not np.isfinite(v).all():
+            raise ParameterError("bias contains non-finite values")
+        self._v = _Dual(v, None)
+
+    @property
+    def values(self) -> np.ndarray:
+        return self._v.host()
+
+    @property
+    def device_values(self) -> torch.Tensor:
+        return self._v.dev()
+
+    def __len__(self) -> int:
+        return self._v.shape()[0]
+
+    def __eq__(self, other) -> bool:
+        return isinstance(other, BiasVector) and np.array_equal(self.values, other.values)
+
+
+def as_ternary(W) -> TernaryDense:
+    return W if isinstance(W, TernaryDense) else TernaryDense(W)
+
+
+def as_dense(X) -> DenseMatrix:
+    if isinstance(X, DenseMatrix):
+        return X
+    if hasattr(X, "values") and not _is_tensor(X) and not isinstance(X, np.ndarray):
+        return DenseMatrix(X.values)  # e.g. the reference's own DenseMatrix
+    return DenseMatrix(X)
+
+
+def as_bias(b) -> BiasVector:
+    if isinstance(b, BiasVector):
+        return b
+    if hasattr(b, "values") and not _is_tensor(b) and not isinstance(b, np.ndarray):
+        return BiasVector(b.values)
+    return BiasVector(b)
+
+
+def prelu(v, alpha: float):
+    """dense.py:184-189: v if v > 0 else alpha * v (host helper)."""
+    if np.isscalar(v):
+        return v if v > 0 else type(v)(alpha * v)
+    arr = np.asarray(v)
+    return np.where(arr > 0, arr, np.float32(alpha) * arr).astype(arr.dtype)
+
+
+def oracle_gemm(X, W, b, alpha: float | None = None) -> DenseMatrix:
+    """dense.py:192-213 semantics: fp64 X @ W + b, PReLU in fp64, one cast to fp32.
+
+    Runs as an fp64 cuBLAS GEMM on the device (a verification utility for
+    the harness, not the ternary hot path)."""
+    X, W, b = as_dense(X), as_ternary(W), as_bias(b)
+    if X.cols != W.K:
+        raise ParameterError(f"X has {X.cols} columns but W has {W.K} rows")
+    if len(b) != W.N:
+        raise ParameterError(f"bias length {len(b)} != N = {W.N}")
+    y = X.device_values.double() @ W.device_values.double() + b.device_values.double()
+    if alpha is not None:
+        y = torch.where(y > 0, y, float(alpha) * y)
+    return DenseMatrix(y.float())

@@ -1,0 +1,98 @@
+"""Cost model and verify-then-time mechanics of the reference harness
+(reference: bench.py:53-73 flop_count / operational_intensity, bench.py:135-206
+_verify / run_point), adapted to device timing.
+
+The grid search, presets and CSV plumbing of the reference harness tune CPU
+unroll factors and are out of scope.
+"""
+
+from __future__ import annotations
+
+import statistics
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .errors import ParameterError, VerificationError
+
+VERIFY_RTOL = 1e-5  # reference bench.py:49; applied normwise / |terms|-scaled, see verify()
+
+
+def flop_count(M: int, K: int, N: int, nnz: int) -> int:
+    """bench.py:53-61: M*N bias adds + one add per (row, nonzero)."""
+    if M < 1 or K < 1 or N < 1:
+        raise ParameterError(f"dimensions must be >= 1, got M={M} K={K} N={N}")
+    if not 0 <= nnz <= K * N:
+        raise ParameterError(f"nnz = {nnz} outside [0, K*N = {K * N}]")
+    return M * N + M * nnz
+
+
+def operational_intensity(M: int, K: int, N: int, nnz: int, format_bytes: int) -> float:
+    """bench.py:64-73: flops / (format bytes + 4MK + 4MN + 4N)."""
+    if format_bytes < 0:
+        raise ParameterError(f"format_bytes must be >= 0, got {format_bytes}")
+    return flop_count(M, K, N, nnz) / (format_bytes + 4 * M * K + 4 * M * N + 4 * N)
+
+
+@dataclass(frozen=True)
+class Agreement:
+    exact: bool
+    normwise: float
+    scaled: float
+    rtol_fails: int  # the reference's own elementwise rtol=1e-5, atol=0 check (reported, not gated)
+
+
+def agreement(y: np.ndarray, ref: np.ndarray, scale: np.ndarray | None = None) -> Agreement:
+    """Parity predicates of SURVEY.md 8(c): bit-exact / normwise / |terms|-scaled."""
+    y64 = np.asarray(y, np.float64)
+    r64 = np.asarray(ref, np.float64)
+    err = np.abs(y64 - r64)
+    den = np.abs(r64).max() if r64.size else 0.0
+    normwise = float(err.max() / den) if den > 0 else float(err.max() if err.size else 0.0)
+    if scale is None:
+        scaled = float("nan")
+    else:
+        with np.errstate(divide="ignore", invalid="ignore"):
+            q = np.where(scale > 0, err / scale, np.where(err > 0, np.inf, 0.0))
+        scaled = float(q.max()) if q.size else 0.0
+    fails = int((~np.isclose(y64, r64, rtol=VERIFY_RTOL, atol=0.0)).sum())
+    return Agreement(bool(np.array_equal(np.asarray(y), np.asarray(ref))), normwise, scaled, fails)
+
+
+def verify(y: np.ndarray, ref: np.ndarray, exact: bool, label: str, tol: float = 1e-5,
+           scale: np.ndarray | None = None) -> Agreement:
+    """Refuse to time a wrong kernel (bench.py:135-150, 167-169).
+
+    exact=True (integer regime): bit equality.  Otherwise normwise error
+    <= tol and, when the |terms| scale is given, scaled error <= tol (the
+    reference's elementwise rtol check is unsatisfiable for real X even by the
+    reference itself)."""
+    a = agreement(y, ref, scale)
+    ok = a.exact if exact else (a.normwise <= tol and (scale is None or a.scaled <= tol))
+    if not ok:
+        raise VerificationError(f"{label} disagrees with the oracle: {a}")
+    return a
+
+
+def time_device(fn, reps: int, warmup: int = 3, flush: torch.Tensor | None = None) -> list[float]:
+    """Per-call device time (ms) with CUDA events on the current stream; the L2
+    is flushed (``flush`` written) before every timed call, outside the events."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    out = []
+    for _ in range(reps):
+        if flush is not None:
+            flush.add_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        out.append(e0.elapsed_time(e1))
+    return out
+
+
+def median(xs) -> float:
+    return float(statistics.median(xs))

@@ -1,0 +1,457 @@
+"""GEMM entry points and the variant registry (reference: kernels/__init__.py,
+kernels/scalar.py, kernels/simd.py) — same names, signatures, argument
+checks and exception types; every call launches sm_100a kernels.
+
+Two device paths serve every entry point (choose with ``GemmConfig(method=)``
+or the ``method=`` keyword; "auto" picks by density):
+
+  "gather"  CUDA-core walk of the format's own index stream, one fp32 lane per
+            output element in the reference kernel's exact operation order —
+            bit-identical to the reference for any finite X (csrc/tg_gather.cu).
+  "mma"     dense-decode tensor-core path: the format is re-encoded once into
+            2-bit ternary tiles, X is split into three exact int8 limbs and
+            tcgen05.mma.kind::i8 accumulates in TMEM (csrc/tg_mma.cu).  Exact
+            integer accumulation; bit-identical to the reference for
+            integer-valued X, ~1e-7 normwise for real X (tolerance 1e-5).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass, replace
+from typing import Any, Callable, NamedTuple
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .dense import BiasVector, DenseMatrix, TernaryDense, _Dual, _device, as_bias, as_dense, as_ternary
+from .errors import ParameterError
+from .formats import (
+    DEFAULT_GROUP_SIMD,
+    BlockedTcsc,
+    InterleavedBlockedTcsc,
+    Tcsc,
+    blocked_from_dense,
+    interleaved_blocked_from_dense,
+    tcsc_from_dense,
+)
+
+DEFAULT_UF = 12
+DEFAULT_MR = 4
+DEFAULT_NR = 4
+ALLOWED_ROW_UNROLL = (1, 2, 4)
+DEFAULT_ALPHA = 0.25
+METHODS = ("auto", "gather", "mma")
+# "auto" uses the tensor-core path when at least 1 in AUTO_MMA_MIN_DENSITY_INV
+# entries of W is nonzero (dense MACs per useful add <= 64).
+AUTO_MMA_MIN_DENSITY_INV = 64
+
+
+class OpCount(NamedTuple):
+    """Floating point operation counters (kernels/scalar.py:51-55)."""
+
+    adds: int
+    mults: int
+
+
+@dataclass(frozen=True)
+class GemmConfig:
+    """Tuning knobs (kernels/scalar.py:58-94) plus ``method`` (device path)."""
+
+    uf: int = DEFAULT_UF
+    mr: int = DEFAULT_MR
+    nr: int = DEFAULT_NR
+    b: int | None = None
+    g: int | None = None
+    alpha: float | None = None
+    variant: str = ""
+    method: str = "auto"
+
+    def __post_init__(self):
+        if self.uf < 1:
+            raise ParameterError(f"uf must be >= 1, got {self.uf}")
+        if self.mr not in ALLOWED_ROW_UNROLL:
+            raise ParameterError(f"mr must be one of {ALLOWED_ROW_UNROLL}, got {self.mr}")
+        if self.nr not in ALLOWED_ROW_UNROLL:
+            raise ParameterError(f"nr must be one of {ALLOWED_ROW_UNROLL}, got {self.nr}")
+        if self.b is not None and self.b < 1:
+            raise ParameterError(f"b must be >= 1, got {self.b}")
+        if self.g is not None and self.g < 1:
+            raise ParameterError(f"g must be >= 1, got {self.g}")
+        if self.alpha is not None and not np.isfinite(self.alpha):
+            raise ParameterError(f"alpha must be finite, got {self.alpha}")
+        if self.method not in METHODS:
+            raise ParameterError(f"method must be one of {METHODS}, got {self.method!r}")
+
+    def with_variant(self, tag: str) -> "GemmConfig":
+        return replace(self, variant=tag)
+
+
+class PaddedInput:
+    """M x (K+1) float32 matrix whose last column is zero (simd.py:40-70)."""
+
+    def __init__(self, values):
+        if isinstance(values, torch.Tensor):
+            v = values.detach()
+            if v.dim() != 2 or v.shape[1] < 1:
+                raise ParameterError(f"padded input must be 2-D with >= 1 column, got {tuple(v.shape)}")
+            v = v.float().contiguous()
+            if not bool(torch.isfinite(v).all().item()):
+                raise ParameterError("padded input contains non-finite values")
+            if v.shape[0] and bool((v[:, -1] != 0).any().item()):
+                raise ParameterError("padded slot (last column) must be exactly zero")
+            self._v = _Dual(None, v)
+            return
+        v = np.ascontiguousarray(values, dtype=np.float32)
+        if v.ndim != 2 or v.shape[1] < 1:
+            raise ParameterError(f"padded input must be 2-D with >= 1 column, got {np.asarray(values).shape}")
+        if not np.isfinite(v).all():
+            raise ParameterError("padded input contains non-finite values")
+        if v.shape[0] and (v[:, -1] != 0).any():
+            raise ParameterError("padded slot (last column) must be exactly zero")
+        self._v = _Dual(v, None)
+
+    @classmethod
+    def _trusted(cls, dev: torch.Tensor) -> "PaddedInput":
+        obj = cls.__new__(cls)
+        obj._v = _Dual(None, dev)
+        return obj
+
+    @property
+    def values(self) -> np.ndarray:
+        return self._v.host()
+
+    @property
+    def device_values(self) -> torch.Tensor:
+        return self._v.dev()
+
+    @property
+    def M(self) -> int:
+        return self._v.shape()[0]
+
+    @property
+    def K(self) -> int:
+        return self._v.shape()[1] - 1
+
+    def logical(self) -> DenseMatrix:
+        return DenseMatrix(self.device_values[:, :-1].contiguous())
+
+
+def pad_input(X) -> PaddedInput:
+    """simd.py:72-75, on the device."""
+    X = as_dense(X)
+    x = X.device_values
+    xp = torch.zeros((x.shape[0], x.shape[1] + 1), dtype=torch.float32, device=x.device)
+    xp[:, :-1] = x
+    return PaddedInput._trusted(xp)
+
+
+# ---------------------------------------------------------------- device plumbing
+
+_ws_lock = threading.Lock()
+_ws_cache: dict[tuple[int, int], torch.Tensor] = {}
+
+
+def _stream() -> torch.cuda.Stream:
+    return torch.cuda.current_stream()
+
+
+def _workspace(nbytes: int, dev: torch.device, stream: int) -> torch.Tensor:
+    key = (dev.index if dev.index is not None else torch.cuda.current_device(), stream)
+    with _ws_lock:
+        t = _ws_cache.get(key)
+        if t is None or t.numel() < nbytes:
+            t = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
+            _ws_cache[key] = t
+    return t
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _alpha_args(alpha: float | None) -> tuple[int, float]:
+    """simd.py:85-90."""
+    if alpha is None:
+        return 0, 0.0
+    if not np.isfinite(alpha):
+        raise ParameterError(f"alpha must be finite, got {alpha}")
+    return 1, float(np.float32(alpha))
+
+
+def _check_dims(x_cols: int, K: int, bias_len: int, N: int) -> None:
+    """kernels/scalar.py:97-101."""
+    if x_cols != K:
+        raise ParameterError(f"X has {x_cols} columns but the format has K = {K}")
+    if bias_len != N:
+        raise ParameterError(f"bias length {bias_len} != N = {N}")
+
+
+def _check_padded(Xp: PaddedInput, K: int, bias_len: int, N: int) -> None:
+    """simd.py:78-82."""
+    if Xp.K != K:
+        raise ParameterError(f"padded input has K = {Xp.K} but the format has K = {K}")
+    if bias_len != N:
+        raise ParameterError(f"bias length {bias_len} != N = {N}")
+
+
+def choose_method(method: str, K: int, N: int, nnz: int) -> str:
+    if method not in METHODS:
+        raise ParameterError(f"method must be one of {METHODS}, got {method!r}")
+    if method != "auto":
+        return method
+    if K > (1 << 24):
+        return "gather"
+    return "mma" if nnz * AUTO_MMA_MIN_DENSITY_INV >= K * N else "gather"
+
+
+class GemmRunner:
+    """One resolved GEMM call with its device buffers: ``launch()`` issues only
+    kernel launches (no allocation, no synchronisation), so it can be replayed
+    or captured in a CUDA graph.  Used by every gemm_* entry point."""
+
+    def __init__(self, kind: str, x: torch.Tensor, fmt, bias: torch.Tensor, *, method: str, uf: int = 1,
+                 mr: int = 1, alpha: float | None = None, out: torch.Tensor | None = None,
+                 flags: torch.Tensor | None = None):
+        self.kind = kind
+        self.x = x
+        self.fmt = fmt
+        self.bias = bias
+        self.M, self.ldx = int(x.shape[0]), int(x.shape[1])
+        self.K, self.N = fmt.K, fmt.N
+        self.uf, self.mr = uf, mr
+        self.use_alpha, self.alpha = _alpha_args(alpha)
+        self.method = method
+        dev = x.device
+        self.y = out if out is not None else torch.empty((self.M, self.N), dtype=torch.float32, device=dev)
+        self.flags = flags if flags is not None else torch.zeros(6, dtype=torch.int32, device=dev)
+        self.ws_bytes = nat.load().tg_gemm_workspace_bytes(self.M, self.K, self.N)
+        self.tiles = fmt.tiles() if method == "mma" else None
+        self.exact = self._format_ref() if method == "mma" else None
+        self._ws = None
+
+    def _format_ref(self) -> nat.TgFormatRef:
+        """The format's own arrays, for the exact-order fix-up of wide-range rows."""
+        f, r = self.fmt, nat.TgFormatRef()
+        r.uf, r.mr, r.g, r.B = max(self.uf, 1), max(self.mr, 1), 1, max(getattr(f, "B", f.K), 1)
+        if self.kind in ("base", "unrolled", "blocked"):
+            r.variant = {"base": nat.TG_VARIANT_BASE, "unrolled": nat.TG_VARIANT_UNROLLED,
+                         "blocked": nat.TG_VARIANT_BLOCKED}[self.kind]
+            r.a0, r.a1 = f.device("col_start_pos").data_ptr(), f.device("row_index_pos").data_ptr()
+            r.a2, r.a3 = f.device("col_start_neg").data_ptr(), f.device("row_index_neg").data_ptr()
+        else:
+            r.variant = (nat.TG_VARIANT_VECTORIZED_OPTIMAL if self.kind == "vectorized_optimal"
+                         else nat.TG_VARIANT_INTERLEAVED_BLOCKED)
+            r.g = f.g
+            r.a0, r.a1 = f.device("col_segment_ptr").data_ptr(), f.device("all_indices").data_ptr()
+        return r
+
+    def launch(self, stream: int | None = None, ws: torch.Tensor | None = None) -> None:
+        st = torch.cuda.current_stream().cuda_stream if stream is None else stream
+        if ws is None:
+            ws = self._ws if self._ws is not None else _workspace(self.ws_bytes, self.x.device, st)
+        x, y, b, fl = _p(self.x), _p(self.y), _p(self.bias), _p(self.flags)
+        M, K, N, ldx = self.M, self.K, self.N, self.ldx
+        f = self.fmt
+        if self.method == "mma":
+            nat.call("tg_gemm_tiles", x, M, K, ldx, _p(self.tiles), N, b, y, N, self.use_alpha, self.alpha,
+                     ctypes.byref(self.exact), _p(ws), ws.numel(), fl, st)
+            return
+        if self.kind in ("base", "unrolled"):
+            nat.call("tg_gemm_tcsc", x, M, K, ldx, _p(f.device("col_start_pos")), _p(f.device("row_index_pos")),
+                     _p(f.device("col_start_neg")), _p(f.device("row_index_neg")), N, b, y, N,
+                     0 if self.kind == "base" else self.uf, self.use_alpha, self.alpha, _p(ws), ws.numel(), fl, st)
+        elif self.kind == "blocked":
+            nat.call("tg_gemm_blocked", x, M, K, ldx, f.B, _p(f.device("col_start_pos")),
+                     _p(f.device("row_index_pos")), _p(f.device("col_start_neg")), _p(f.device("row_index_neg")), N,
+                     b, y, N, self.uf, self.mr, self.use_alpha, self.alpha, _p(ws), ws.numel(), fl, st)
+        else:
+            order = (nat.TG_ORDER_VECTORIZED_OPTIMAL if self.kind == "vectorized_optimal"
+                     else nat.TG_ORDER_INTERLEAVED_BLOCKED)
+            nat.call("tg_gemm_interleaved_blocked", x, M, K, ldx, f.B, f.g, _p(f.device("all_indices")),
+                     _p(f.device("col_segment_ptr")), N, b, y, N, order, self.use_alpha, self.alpha, _p(ws),
+                     ws.numel(), fl, st)
+
+    def pin_workspace(self) -> None:
+        """Give this runner a private workspace (needed for graph capture / concurrent replays)."""
+        self._ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, device=self.x.device)
+
+    def result(self) -> DenseMatrix:
+        return DenseMatrix(self.y, _flags=self.flags)
+
+    def nonpositive(self) -> int:
+        f = self.flags.cpu().numpy().view(np.uint32)
+        return int(f[2]) | (int(f[3]) << 32)
+
+
+def _finish(runner: GemmRunner, counted: bool, adds: int):
+    runner.launch()
+    y = runner.result()
+    if not counted:
+        return y
+    mults = runner.nonpositive() if runner.use_alpha else 0
+    return y, OpCount(int(adds), int(mults))
+
+
+def _method(cfg: GemmConfig | None, method: str | None, K: int, N: int, nnz: int) -> str:
+    m = method if method is not None else (cfg.method if cfg is not None else "auto")
+    return choose_method(m, K, N, nnz)
+
+
+# ---------------------------------------------------------------- entry points
+
+
+def _as_tcsc(t) -> Tcsc:
+    if isinstance(t, Tcsc):
+        return t
+    return Tcsc(t.K, t.N, t.col_start_pos, t.row_index_pos, t.col_start_neg, t.row_index_neg)
+
+
+def _as_blocked(t) -> BlockedTcsc:
+    if isinstance(t, BlockedTcsc):
+        return t
+    return BlockedTcsc(t.K, t.N, t.B, t.col_start_pos, t.row_index_pos, t.col_start_neg, t.row_index_neg)
+
+
+def _as_ib(t) -> InterleavedBlockedTcsc:
+    if isinstance(t, InterleavedBlockedTcsc):
+        return t
+    return InterleavedBlockedTcsc(t.K, t.N, t.B, t.g, t.all_indices, t.col_segment_ptr,
+                                  getattr(t, "symmetric_groups", False))
+
+
+def gemm_base(X, t, b, counted: bool = False, *, method: str | None = None):
+    """kernels/scalar.py:135-148.  counted: adds = M*N + M*nnz, mults = 0."""
+    X, b, t = as_dense(X), as_bias(b), _as_tcsc(t)
+    _check_dims(X.cols, t.K, len(b), t.N)
+    m = _method(None, method, t.K, t.N, t.nnz)
+    r = GemmRunner("base", X.device_values, t, b.device_values, method=m)
+    return _finish(r, counted, X.rows * t.N + X.rows * t.nnz)
+
+
+def gemm_unrolled(X, t, b, cfg: GemmConfig | None = None, counted: bool = False, *, method: str | None = None):
+    """kernels/scalar.py:260-278 (uf accumulator banks; mr/nr change no output bit)."""
+    cfg = cfg or GemmConfig()
+    X, b, t = as_dense(X), as_bias(b), _as_tcsc(t)
+    _check_dims(X.cols, t.K, len(b), t.N)
+    m = _method(cfg, method, t.K, t.N, t.nnz)
+    r = GemmRunner("unrolled", X.device_values, t, b.device_values, method=m, uf=cfg.uf)
+    M = X.rows
+    return _finish(r, counted, M * t.nnz + M * t.N * (cfg.uf + 1))
+
+
+def gemm_blocked(X, t, b, cfg: GemmConfig | None = None, counted: bool = False, *, method: str | None = None):
+    """kernels/scalar.py:370-389."""
+    cfg = cfg or GemmConfig()
+    X, b, t = as_dense(X), as_bias(b), _as_blocked(t)
+    _check_dims(X.cols, t.K, len(b), t.N)
+    m = _method(cfg, method, t.K, t.N, t.nnz)
+    r = GemmRunner("blocked", X.device_values, t, b.device_values, method=m, uf=cfg.uf, mr=cfg.mr)
+    M, nb = X.rows, t.num_blocks
+    mf = M // cfg.mr * cfg.mr
+    return _finish(r, counted, M * t.nnz + mf * t.N * nb * (cfg.uf + 1) + (M - mf) * t.N * nb)
+
+
+def gemm_interleaved_blocked(X, t, b, cfg: GemmConfig | None = None, counted: bool = False, *,
+                             method: str | None = None):
+    """kernels/scalar.py:488-511; rejects symmetric formats like the reference (:502-505)."""
+    cfg = cfg or GemmConfig()
+    X, b, t = as_dense(X), as_bias(b), _as_ib(t)
+    _check_dims(X.cols, t.K, len(b), t.N)
+    if t.symmetric_groups:
+        raise ParameterError(
+            "scalar kernel cannot consume symmetric-group formats (dummy index needs a padded input row)"
+        )
+    m = _method(cfg, method, t.K, t.N, t.nnz)
+    r = GemmRunner("interleaved_blocked", X.device_values, t, b.device_values, method=m)
+    M = X.rows
+    return _finish(r, counted, M * t.nnz + M * t.N * t.num_blocks)
+
+
+def gemm_vectorized_optimal(Xp, t, b, alpha: float | None = None, cfg: GemmConfig | None = None,
+                            counted: bool = False, *, method: str | None = None):
+    """kernels/simd.py:423-449: symmetric interleaved-blocked stream + fused bias/PReLU."""
+    if not isinstance(Xp, PaddedInput):
+        Xp = PaddedInput(getattr(Xp, "values", Xp))
+    b, t = as_bias(b), _as_ib(t)
+    _check_padded(Xp, t.K, len(b), t.N)
+    if not t.symmetric_groups:
+        raise ParameterError("gemm_vectorized_optimal needs symmetric 4-column groups (symmetric_cols=True)")
+    if alpha is None and cfg is not None:
+        alpha = cfg.alpha
+    _alpha_args(alpha)
+    n_idx = t._len("all_indices")
+    m = _method(cfg, method, t.K, t.N, n_idx)
+    r = GemmRunner("vectorized_optimal", Xp.device_values, t, b.device_values, method=m, alpha=alpha)
+    return _finish(r, counted, Xp.M * (n_idx + t.N * t.num_blocks))
+
+
+# ---------------------------------------------------------------- registry (kernels/__init__.py:66-230)
+
+
+@dataclass(frozen=True)
+class VariantSpec:
+    """How one variant tag plugs into the harness (kernels/__init__.py:66-80)."""
+
+    tag: str
+    kind: str  # "scalar" or "simd"
+    supports_alpha: bool
+    emit: frozenset
+    build: Callable[[TernaryDense, GemmConfig], Any]
+    prepare: Callable[[DenseMatrix], Any]
+    run: Callable[[Any, Any, BiasVector, GemmConfig, bool], Any]
+
+
+def _identity(x):
+    return as_dense(x)
+
+
+def _g(cfg: GemmConfig, default: int) -> int:
+    return default if cfg.g is None else cfg.g
+
+
+VARIANTS: dict[str, VariantSpec] = {}
+
+
+def _register(spec: VariantSpec) -> None:
+    VARIANTS[spec.tag] = spec
+
+
+_register(VariantSpec("base", "scalar", False, frozenset(), lambda w, cfg: tcsc_from_dense(w), _identity,
+                      lambda x, f, b, cfg, counted: gemm_base(x, f, b, counted, method=cfg.method)))
+_register(VariantSpec("unrolled", "scalar", False, frozenset({"UF", "MR", "NR"}), lambda w, cfg: tcsc_from_dense(w),
+                      _identity, lambda x, f, b, cfg, counted: gemm_unrolled(x, f, b, cfg, counted)))
+_register(VariantSpec("blocked", "scalar", False, frozenset({"UF", "MR", "NR", "B"}),
+                      lambda w, cfg: blocked_from_dense(w, cfg.b), _identity,
+                      lambda x, f, b, cfg, counted: gemm_blocked(x, f, b, cfg, counted)))
+_register(VariantSpec("interleaved_blocked", "scalar", False, frozenset({"MR", "NR", "B", "g"}),
+                      lambda w, cfg: interleaved_blocked_from_dense(w, cfg.b, _g(cfg, DEFAULT_GROUP_SIMD)), _identity,
+                      lambda x, f, b, cfg, counted: gemm_interleaved_blocked(x, f, b, cfg, counted)))
+_register(VariantSpec("vectorized_optimal", "simd", True, frozenset({"B", "g"}),
+                      lambda w, cfg: interleaved_blocked_from_dense(w, cfg.b, _g(cfg, DEFAULT_GROUP_SIMD),
+                                                                    symmetric_cols=True),
+                      pad_input,
+                      lambda x, f, b, cfg, counted: gemm_vectorized_optimal(x, f, b, cfg.alpha, cfg, counted)))
+
+SCALAR_TAGS = tuple(tag for tag, s in VARIANTS.items() if s.kind == "scalar")
+SIMD_TAGS = tuple(tag for tag, s in VARIANTS.items() if s.kind == "simd")
+
+
+def get_variant(tag: str) -> VariantSpec:
+    spec = VARIANTS.get(tag)
+    if spec is None:
+        raise ParameterError(f"unknown variant {tag!r}; known: {', '.join(VARIANTS)}")
+    return spec
+
+
+def run_variant(tag: str, X, W, b, cfg: GemmConfig | None = None, counted: bool = False):
+    """kernels/__init__.py:211-230: build the format, prepare X, run once."""
+    cfg = cfg or GemmConfig()
+    spec = get_variant(tag)
+    if cfg.alpha is not None and not spec.supports_alpha:
+        raise ParameterError(f"variant {tag!r} has no fused PReLU; alpha is vectorized-only")
+    fmt = spec.build(as_ternary(W), cfg)
+    prepared = spec.prepare(as_dense(X))
+    return spec.run(prepared, fmt, as_bias(b), cfg, counted)

@@ -1,0 +1,396 @@
+"""GPU parity: the sm_100a builders and kernels, through the C ABI, against the
+reference (golden fixtures) and the pinned CPU oracle.
+
+Bars:
+  * index arrays of every format: bit-exact;
+  * gather path: Y bit-exact with the reference kernel for ANY finite X
+    (same fp32 operation order);
+  * tensor-core path: bit-exact for integer-valued X; for real X normwise
+    max|dY|/max|Y| <= 1e-5 and |dY| <= 1e-5 * (sum_k |x||w| + |b|) elementwise.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import parse_opt, worked_example
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def tg():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2510_06957_b200 as m
+
+    return m
+
+
+def _fmt_arrays(golden, prefix):
+    return {k.split(".")[-1]: golden[k] for k in golden.npz.files if k.startswith(prefix + ".")}
+
+
+def _assert_tol(y, X, W, b, alpha=None, label=""):
+    ref = orc.oracle_gemm(X, W, b, alpha)
+    nw = orc.normwise_error(y, ref)
+    sc = orc.scaled_error(y, X, W, b, alpha)
+    assert nw <= TOL and sc <= TOL, (label, nw, sc)
+    return nw, sc
+
+
+# ---------------------------------------------------------------- builders
+
+
+def test_builders_bit_exact_vs_reference(tg, golden_formats):
+    n = 0
+    for entry in golden_formats.index:
+        key = entry["key"]
+        W = golden_formats[f"{key}.W"]
+        t = tg.tcsc_from_dense(W)
+        for name, arr in _fmt_arrays(golden_formats, f"{key}.tcsc").items():
+            assert np.array_equal(getattr(t, name), arr), (key, "tcsc", name)
+        for f in entry["formats"][1:]:
+            ref = _fmt_arrays(golden_formats, f"{key}.{f['name']}")
+            if f["name"].startswith("blocked"):
+                got = tg.blocked_from_dense(W, f["B"])
+            else:
+                got = tg.interleaved_blocked_from_dense(W, f["B"], f["g"], f["sym"])
+                assert got.format_bytes() == f["bytes"]
+                assert got.nnz == f["nnz"]
+            assert got.B == f["resolved_B"]
+            for name, arr in ref.items():
+                assert np.array_equal(getattr(got, name), arr), (key, f["name"], name)
+            n += 1
+    assert n > 500
+
+
+def test_builders_device_resident_input(tg):
+    rng = np.random.default_rng(3)
+    W = rng.integers(-1, 2, size=(300, 64)).astype(np.int8)
+    dW = torch.from_numpy(W).cuda()
+    t = tg.interleaved_blocked_from_dense(tg.TernaryDense(dW), 64, 2, True)
+    ref = orc.interleaved_blocked_from_dense(W, 64, 2, True)
+    assert np.array_equal(t.all_indices, ref["all_indices"])
+    assert np.array_equal(t.col_segment_ptr, ref["col_segment_ptr"])
+
+
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg4"])
+def test_builders_full_size(tg, cfg):
+    from paper_2510_06957_b200.workloads import make_inputs
+
+    W, _, _ = make_inputs(cfg, M=1)
+    dW = tg.TernaryDense(torch.from_numpy(W).cuda())
+    ref = orc.interleaved_blocked_from_dense(W, None, 2, True)
+    got = tg.interleaved_blocked_from_dense(dW, None, 2, True)
+    assert np.array_equal(got.all_indices, ref["all_indices"])
+    assert np.array_equal(got.col_segment_ptr, ref["col_segment_ptr"])
+    reft = orc.tcsc_from_dense(W)
+    t = tg.tcsc_from_dense(dW)
+    for name in ("col_start_pos", "row_index_pos", "col_start_neg", "row_index_neg"):
+        assert np.array_equal(getattr(t, name), reft[name])
+    bl = tg.blocked_from_dense(dW, 1000)
+    refb = orc.blocked_from_dense(W, 1000)
+    for name in ("col_start_pos", "row_index_pos", "col_start_neg", "row_index_neg"):
+        assert np.array_equal(getattr(bl, name), refb[name])
+
+
+def test_round_trips(tg, golden_formats):
+    for entry in golden_formats.index[:30]:
+        W = golden_formats[f"{entry['key']}.W"]
+        assert np.array_equal(tg.tcsc_from_dense(W).to_dense().values, W)
+        assert np.array_equal(tg.blocked_from_dense(W, 3).to_dense().values, W)
+        sym = W.shape[1] % 4 == 0
+        assert np.array_equal(tg.interleaved_blocked_from_dense(W, 5, 2, sym).to_dense().values, W)
+
+
+def test_builder_rejects_bad_entries(tg):
+    W = torch.zeros((5, 4), dtype=torch.int8, device="cuda")
+    W[3, 2] = 2
+    with pytest.raises(tg.ParameterError, match=r"entry \(3, 2\) = 2"):
+        tg.tcsc_from_dense(tg.TernaryDense(W))
+    with pytest.raises(tg.ParameterError):
+        tg.TernaryDense(np.array([[0, 3]]))
+    with pytest.raises(tg.ParameterError):
+        tg.interleaved_blocked_from_dense(np.zeros((4, 6), np.int8), symmetric_cols=True)
+
+
+def test_corruption_detected(tg):
+    # tcsc.py:95-114: a cell in both sign arrays / duplicate rows -> CorruptionError
+    t = tg.Tcsc(3, 1, [0, 1], [1], [0, 1], [1])
+    with pytest.raises(tg.CorruptionError):
+        t.to_dense()
+    t2 = tg.Tcsc(3, 1, [0, 2], [1, 1], [0, 0], [])
+    with pytest.raises(tg.CorruptionError):
+        t2.to_dense()
+    assert tg.validate(t) == ["cell (1, 0) appears in both sign arrays"]
+    assert tg.validate(t2) == ["row_index_pos not strictly increasing in column 0"]
+    assert tg.validate(tg.tcsc_from_dense(np.array([[1, 0], [0, -1], [-1, 0], [1, 0]], np.int8))) == []
+
+
+# ---------------------------------------------------------------- kernels vs reference
+
+
+def _run_golden(tg, golden, entry, run, method):
+    key = entry["key"]
+    W, X, b = golden[f"{key}.W"], golden[f"{key}.X"], golden[f"{key}.b"]
+    name = run["name"]
+    if name == "base":
+        return tg.gemm_base(X, tg.tcsc_from_dense(W), b, counted=True, method=method)
+    if name.startswith("unrolled"):
+        cfg = tg.GemmConfig(uf=run["uf"], mr=run["mr"], nr=run["nr"])
+        return tg.gemm_unrolled(X, tg.tcsc_from_dense(W), b, cfg, counted=True, method=method)
+    if name.startswith("blocked"):
+        cfg = tg.GemmConfig(uf=run["uf"], mr=run["mr"], b=parse_opt(run["B"]))
+        return tg.gemm_blocked(X, tg.blocked_from_dense(W, parse_opt(run["B"])), b, cfg, counted=True, method=method)
+    if name.startswith("ib"):
+        cfg = tg.GemmConfig(mr=run["mr"], b=parse_opt(run["B"]), g=run["g"])
+        f = tg.interleaved_blocked_from_dense(W, parse_opt(run["B"]), run["g"])
+        return tg.gemm_interleaved_blocked(X, f, b, cfg, counted=True, method=method)
+    f = tg.interleaved_blocked_from_dense(W, parse_opt(run["B"]), run["g"], True)
+    return tg.gemm_vectorized_optimal(tg.pad_input(X), f, b, run["alpha"], counted=True, method=method)
+
+
+def test_gather_bit_exact_vs_reference_any_x(tg, golden_kernels):
+    """Every reference kernel, integer AND real X: identical bits."""
+    for entry in golden_kernels.index:
+        for run in entry["runs"]:
+            y, ops = _run_golden(tg, golden_kernels, entry, run, "gather")
+            ref = golden_kernels[f"{entry['key']}.{run['name']}"]
+            assert np.array_equal(y.values.view(np.uint32), ref.view(np.uint32)), (entry["key"], run["name"])
+            assert ops.adds == run["adds"], (entry["key"], run["name"], ops.adds, run["adds"])
+            assert ops.mults == run["mults"], (entry["key"], run["name"])
+
+
+def test_mma_vs_reference(tg, golden_kernels):
+    for entry in golden_kernels.index:
+        key = entry["key"]
+        W, X, b = golden_kernels[f"{key}.W"], golden_kernels[f"{key}.X"], golden_kernels[f"{key}.b"]
+        for run in entry["runs"]:
+            y, ops = _run_golden(tg, golden_kernels, entry, run, "mma")
+            alpha = run.get("alpha")
+            if entry["xmode"] == "int":
+                ref = golden_kernels[f"{key}.{run['name']}"]
+                assert np.array_equal(y.values, ref), (key, run["name"])
+                assert ops.mults == run["mults"]
+            else:
+                _assert_tol(y.values, X, W, b, alpha, (key, run["name"]))
+            assert ops.adds == run["adds"]
+
+
+def test_worked_example_all_variants_both_paths(tg):
+    W, X, b = worked_example()
+    for method in ("gather", "mma"):
+        for tag in tg.SCALAR_TAGS:
+            y = tg.run_variant(tag, X, W, b, tg.GemmConfig(method=method))
+            assert y.values.tolist() == [[12.0, 18.0]], (tag, method)
+    W4 = np.zeros((4, 4), np.int8)
+    W4[:, :2] = W
+    for method in ("gather", "mma"):
+        y = tg.run_variant("vectorized_optimal", X, W4, np.array([10, 20, 0, -1], np.float32),
+                           tg.GemmConfig(alpha=0.5, method=method))
+        assert y.values.tolist() == [[12.0, 18.0, 0.0, -0.5]]
+
+
+# ---------------------------------------------------------------- BASELINE configs at full size
+
+
+def test_cfg1_full(tg, golden_cfg1):
+    from paper_2510_06957_b200.workloads import make_inputs
+
+    W, X, b = make_inputs("cfg1")
+    t = tg.tcsc_from_dense(W)
+    for name in ("col_start_pos", "col_start_neg", "row_index_pos", "row_index_neg"):
+        assert np.array_equal(getattr(t, name), golden_cfg1[name])
+    y = tg.gemm_base(X, t, b, method="gather").values
+    assert np.array_equal(y, golden_cfg1["Y_base"])
+    y2 = tg.gemm_base(X, t, b, method="mma").values
+    _assert_tol(y2, X, W, b)
+
+
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg4"])
+def test_vectorized_optimal_full_size(tg, cfg):
+    from paper_2510_06957_b200.workloads import WORKLOADS, make_inputs
+
+    wl = WORKLOADS[cfg]
+    W, X, b = make_inputs(cfg)
+    t = tg.interleaved_blocked_from_dense(torch.from_numpy(W).cuda(), None, 2, True)
+    Xp = tg.pad_input(torch.from_numpy(X).cuda())
+    ref_t = orc.interleaved_blocked_from_dense(W, None, 2, True)
+    ref = orc.gemm_vectorized_optimal(orc.pad_input(X), ref_t, b, wl.alpha, threads=8)
+    yg = tg.gemm_vectorized_optimal(Xp, t, b, wl.alpha, method="gather").values
+    assert np.array_equal(yg, ref)
+    ym = tg.gemm_vectorized_optimal(Xp, t, b, wl.alpha, method="mma").values
+    _assert_tol(ym, X, W, b, wl.alpha, cfg)
+    # integer twin: both paths bit-exact with the reference order
+    Wi, Xi, bi = make_inputs(cfg, integer=True)
+    Xpi = tg.pad_input(Xi)
+    refi = orc.gemm_vectorized_optimal(orc.pad_input(Xi), ref_t, bi, wl.alpha, threads=8)
+    assert np.array_equal(tg.gemm_vectorized_optimal(Xpi, t, bi, wl.alpha, method="mma").values, refi)
+    assert np.array_equal(tg.gemm_vectorized_optimal(Xpi, t, bi, wl.alpha, method="gather").values, refi)
+
+
+@pytest.mark.parametrize("s", ["s1_16", "s1_2"])
+def test_cfg3_sweep_points(tg, s):
+    from paper_2510_06957_b200.workloads import make_inputs
+
+    name = f"cfg3_{s}"
+    W, X, b = make_inputs(name)
+    dW = torch.from_numpy(W).cuda()
+    t = tg.interleaved_blocked_from_dense(dW, None, 2)
+    ym = tg.gemm_interleaved_blocked(X, t, b, method="mma")
+    yv = ym.device_values
+    ref = (torch.from_numpy(X).cuda().double() @ dW.double() + torch.from_numpy(b).cuda().double())
+    nw = float((yv.double() - ref).abs().max() / ref.abs().max())
+    assert nw <= TOL
+    # gather path, bit-exact with the reference order on a row slice (C oracle, 8 threads)
+    rows = slice(0, 16)
+    ref_t = orc.interleaved_blocked_from_dense(W, None, 2)
+    ref_rows = orc.gemm_interleaved_blocked(X[rows], ref_t, b, threads=8)
+    yg = tg.gemm_interleaved_blocked(X[rows], t, b, method="gather").values
+    assert np.array_equal(yg, ref_rows)
+
+
+def test_cfg5_rows_are_independent_and_match_oracle(tg):
+    """cfg5 at full size on the tensor-core path; the seeded 256-row slice is
+    checked against the oracle, and rows computed in the full run equal the
+    same rows computed alone (per-row limb scaling makes rows independent)."""
+    from paper_2510_06957_b200.workloads import cfg5_oracle_rows, make_inputs
+
+    W, X, b = make_inputs("cfg5")
+    dW = torch.from_numpy(W).cuda()
+    t = tg.interleaved_blocked_from_dense(tg.TernaryDense(dW), None, 2)
+    dX = torch.from_numpy(X).cuda()
+    y = tg.gemm_interleaved_blocked(dX, t, b, method="mma").device_values
+    rows = cfg5_oracle_rows()
+    ys = tg.gemm_interleaved_blocked(dX[torch.from_numpy(rows).cuda()], t, b, method="mma").device_values
+    assert torch.equal(y[torch.from_numpy(rows).cuda()], ys)
+    ref = (dX[torch.from_numpy(rows).cuda()].double() @ dW.double() + torch.from_numpy(b).cuda().double())
+    nw = float((ys.double() - ref).abs().max() / ref.abs().max())
+    assert nw <= TOL
+    del y, ys, ref
+
+
+# ---------------------------------------------------------------- edge cases
+
+
+@pytest.mark.parametrize("M,K,N", [(1, 1, 1), (1, 1, 4), (2, 129, 3), (17, 127, 129), (33, 256, 255), (65, 130, 260),
+                                   (129, 1000, 8)])
+@pytest.mark.parametrize("method", ["gather", "mma"])
+def test_odd_shapes(tg, M, K, N, method):
+    rng = np.random.default_rng(M * 1000 + K + N)
+    W = rng.integers(-1, 2, size=(K, N)).astype(np.int8)
+    Xi = rng.integers(-8, 9, size=(M, K)).astype(np.float32)
+    bi = rng.integers(-8, 9, size=N).astype(np.float32)
+    for tag in tg.SCALAR_TAGS:
+        y = tg.run_variant(tag, Xi, W, bi, tg.GemmConfig(method=method, b=7, uf=3, mr=2)).values
+        assert np.array_equal(y, orc.oracle_gemm(Xi, W, bi)), (tag, method)
+    Xr = rng.standard_normal((M, K)).astype(np.float32)
+    t = tg.tcsc_from_dense(W)
+    y = tg.gemm_base(Xr, t, bi, method=method).values
+    if method == "gather":
+        assert np.array_equal(y, orc.gemm_base(Xr, orc.tcsc_from_dense(W), bi))
+    else:
+        _assert_tol(y, Xr, W, bi)
+
+
+@pytest.mark.parametrize("method", ["gather", "mma"])
+def test_degenerate_matrices(tg, method):
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((9, 40)).astype(np.float32)
+    b = rng.standard_normal(8).astype(np.float32)
+    for W in (np.zeros((40, 8), np.int8), np.ones((40, 8), np.int8), -np.ones((40, 8), np.int8)):
+        y = tg.run_variant("base", X, W, b, tg.GemmConfig(method=method)).values
+        _assert_tol(y, X, W, b)
+    # all-zero X rows and a zero bias
+    X0 = np.zeros((3, 40), np.float32)
+    W = rng.integers(-1, 2, (40, 8)).astype(np.int8)
+    assert np.array_equal(tg.run_variant("base", X0, W, np.zeros(8, np.float32),
+                                         tg.GemmConfig(method=method)).values, np.zeros((3, 8), np.float32))
+
+
+def test_wide_dynamic_range_rows_take_exact_fixup(tg):
+    """Rows whose entries span many binades are recomputed in the reference's
+    exact order: bit-identical with the reference kernel even on the mma path."""
+    rng = np.random.default_rng(5)
+    M, K, N = 40, 3000, 64
+    W = rng.integers(-1, 2, size=(K, N)).astype(np.int8)
+    X = rng.standard_normal((M, K)).astype(np.float32)
+    X[3, 17] = 1e6
+    X[7, :] *= np.float32(1e-30)
+    X[7, 5] = 3e-20
+    X[11, ::3] = 0.0
+    X[11, 0] = 5e4
+    b = rng.standard_normal(N).astype(np.float32)
+    t = tg.interleaved_blocked_from_dense(W, None, 2, True)
+    ref_t = orc.interleaved_blocked_from_dense(W, None, 2, True)
+    ref = orc.gemm_vectorized_optimal(orc.pad_input(X), ref_t, b, 0.25)
+    y, ops = tg.gemm_vectorized_optimal(tg.pad_input(X), t, b, 0.25, method="mma", counted=True)
+    y = y.values
+    for r in (3, 7, 11):
+        assert np.array_equal(y[r], ref[r]), r
+    _assert_tol(y, X, W, b, 0.25)
+    ref_lin = orc.oracle_gemm(X, W, b)
+    assert abs(ops.mults - int((ref_lin <= 0).sum())) <= 2
+
+
+def test_extreme_magnitudes(tg):
+    rng = np.random.default_rng(8)
+    W = rng.integers(-1, 2, size=(256, 16)).astype(np.int8)
+    for scale in (1e-30, 1e-10, 1e10, 1e30):
+        X = (rng.standard_normal((5, 256)) * scale).astype(np.float32)
+        b = np.zeros(16, np.float32)
+        y = tg.gemm_base(X, tg.tcsc_from_dense(W), b, method="mma").values
+        _assert_tol(y, X, W, b, label=scale)
+
+
+def test_errors_match_reference(tg):
+    W, X, b = worked_example()
+    t = tg.tcsc_from_dense(W)
+    with pytest.raises(tg.ParameterError):
+        tg.gemm_base(np.ones((1, 3), np.float32), t, b)
+    with pytest.raises(tg.ParameterError):
+        tg.gemm_base(X, t, np.ones(3, np.float32))
+    ib_sym = tg.interleaved_blocked_from_dense(np.zeros((4, 4), np.int8), symmetric_cols=True)
+    with pytest.raises(tg.ParameterError):
+        tg.gemm_interleaved_blocked(X, ib_sym, np.zeros(4, np.float32))
+    plain = tg.interleaved_blocked_from_dense(np.zeros((4, 4), np.int8))
+    with pytest.raises(tg.ParameterError):
+        tg.gemm_vectorized_optimal(tg.pad_input(X), plain, np.zeros(4, np.float32))
+    with pytest.raises(tg.ParameterError):
+        tg.gemm_vectorized_optimal(tg.pad_input(X), ib_sym, np.zeros(4, np.float32), float("inf"))
+    with pytest.raises(tg.ParameterError):
+        tg.run_variant("base", X, W, b, tg.GemmConfig(alpha=0.25))
+    with pytest.raises(tg.ParameterError):
+        tg.run_variant("nope", X, W, b)
+    with pytest.raises(tg.ParameterError):
+        tg.DenseMatrix(np.array([[np.nan]], np.float32))
+
+
+def test_nonfinite_output_is_reported(tg):
+    W = np.ones((2, 1), np.int8)
+    X = np.array([[3e38, 3e38]], np.float32)
+    y = tg.gemm_base(X, tg.tcsc_from_dense(W), np.zeros(1, np.float32), method="gather")
+    with pytest.raises(tg.ParameterError, match="non-finite"):
+        y.values
+
+
+def test_padded_input_dummy_slot(tg):
+    """simd.py:40-75: a corrupted pad slot changes the gather result when dummies exist."""
+    v = np.zeros((12, 4), np.int8)
+    v[0:3, 0] = 1
+    v[3:6, 0] = -1
+    v[0, 1] = 1
+    X = np.arange(24, dtype=np.float32).reshape(2, 12)
+    b = np.zeros(4, np.float32)
+    t = tg.interleaved_blocked_from_dense(v, None, 2, True)
+    assert int((torch.from_numpy(t.all_indices) == 12).sum()) > 0
+    clean = tg.gemm_vectorized_optimal(tg.pad_input(X), t, b, method="gather").values
+    assert np.array_equal(clean, orc.oracle_gemm(X, v, b))
+    with pytest.raises(tg.ParameterError):
+        tg.PaddedInput(np.ones((2, 13), np.float32))

@@ -1,0 +1,156 @@
+"""Host-side logic that needs no GPU: configuration checks, the registry
+contract, the cost model, the workload generator pins and the C-ABI symbol
+table of the built library (loaded, no compute calls)."""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import paper_2510_06957_b200 as tg
+from paper_2510_06957_b200 import _native
+from paper_2510_06957_b200.workloads import WORKLOADS, algorithmic_bytes, cfg5_oracle_rows, make_inputs, ops
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_config_validation_matches_reference():
+    # kernels/scalar.py:79-91
+    for bad in (dict(uf=0), dict(mr=3), dict(nr=8), dict(b=0), dict(g=0), dict(alpha=float("nan")),
+                dict(method="cpu")):
+        with pytest.raises(tg.ParameterError):
+            tg.GemmConfig(**bad)
+    cfg = tg.GemmConfig().with_variant("base")
+    assert cfg.variant == "base" and cfg.uf == 12 and cfg.mr == 4 and cfg.nr == 4 and cfg.b is None
+
+
+def test_registry_contract():
+    # kernels/__init__.py:66-80, 200-208: same tags, kinds and alpha support
+    assert tg.SCALAR_TAGS == ("base", "unrolled", "blocked", "interleaved_blocked")
+    assert tg.SIMD_TAGS == ("vectorized_optimal",)
+    for tag, spec in tg.VARIANTS.items():
+        assert spec.tag == tag
+        assert spec.supports_alpha == (tag == "vectorized_optimal")
+    assert tg.get_variant("blocked").emit == frozenset({"UF", "MR", "NR", "B"})
+    with pytest.raises(tg.ParameterError):
+        tg.get_variant("inverted")
+
+
+def test_cost_model_pins():
+    # pkg/tests/test_bench.py:23-27 and 45-56
+    assert tg.flop_count(32, 1024, 1024, 1024 * 256) == 8_421_376
+    assert tg.flop_count(64, 4096, 4096, 4096 * 2048) == 537_133_056
+    assert tg.flop_count(3, 10, 4, 0) == 12
+    with pytest.raises(tg.ParameterError):
+        tg.flop_count(0, 1, 1, 0)
+    with pytest.raises(tg.ParameterError):
+        tg.flop_count(1, 2, 2, 5)
+    oi = tg.operational_intensity(64, 1024, 1024, 1024 * 512, tg.tcsc_bytes_for(1024, 1024, 1024 * 512))
+    assert abs(oi - 12.77) < 0.01
+    assert oi == 33_619_968 / 2_633_736
+    assert tg.tcsc_bytes_for(4, 2, 4) == 40
+    assert tg.tcsc_bytes_for(1024, 1024, 524_288) == 2_105_352
+    with pytest.raises(tg.ParameterError):
+        tg.tcsc_bytes_for(2, 2, 5)
+
+
+def test_block_size_resolution():
+    assert tg.resolve_block_size(None, 100) == 100
+    assert tg.resolve_block_size(None, 10_000) == 4096
+    assert tg.resolve_block_size(7, 100) == 7
+    with pytest.raises(tg.ParameterError):
+        tg.resolve_block_size(0, 5)
+
+
+def test_workload_recipe_pins():
+    # cfg1 generator pin (seed 1)
+    import hashlib
+
+    W, X, b = make_inputs("cfg1")
+    h = lambda a: hashlib.sha256(a.tobytes()).hexdigest()[:16]  # noqa: E731
+    assert (h(W), h(X), h(b)) == ("056a3b1eb0c433eb", "3d06f7c898896916", "3af6b41d0defe22c")
+    assert int(np.count_nonzero(W)) == 131163
+    assert ops(64, 512, 131163) == 64 * 512 + 64 * 131163
+    rows = cfg5_oracle_rows()
+    assert rows.shape == (256,) and np.all(np.diff(rows) > 0) and rows.max() < 8192
+    assert set(WORKLOADS) >= {"cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "cfg3_s1_16", "cfg3_s1_8", "cfg3_s1_4"}
+    assert WORKLOADS["cfg3_s1_16"].p_pos == float(Fraction(1, 32))
+    assert algorithmic_bytes(256, 4096, 4096, 8_388_608) == 4 * (2 * 4097 + 8_388_608) + 4 * 256 * 4096 * 2 + 4 * 4096
+
+
+def test_integer_twin_keeps_w():
+    W, X, b = make_inputs("cfg1")
+    Wi, Xi, bi = make_inputs("cfg1", integer=True)
+    assert np.array_equal(W, Wi)
+    assert np.all(Xi == np.round(Xi)) and np.abs(Xi).max() <= 8
+
+
+def test_host_types_validate_like_reference():
+    with pytest.raises(tg.ParameterError, match=r"entry \(0, 1\) = 2 is not in"):
+        tg.TernaryDense(np.array([[0, 2]]))
+    with pytest.raises(tg.ParameterError):
+        tg.TernaryDense(np.zeros((0, 3)))
+    with pytest.raises(tg.ParameterError):
+        tg.DenseMatrix(np.array([1.0, 2.0]))
+    with pytest.raises(tg.ParameterError):
+        tg.BiasVector(np.array([np.inf], np.float32))
+    with pytest.raises(tg.ParameterError):
+        tg.PaddedInput(np.ones((2, 3), np.float32))
+    p = tg.PaddedInput(np.array([[1.0, 2.0, 0.0]], np.float32))
+    assert (p.M, p.K) == (1, 2)
+    w = tg.TernaryDense(np.array([[1, 0], [0, -1], [-1, 0], [1, 0]]))
+    assert (w.K, w.N, w.nnz) == (4, 2, 4)
+    assert tg.prelu(np.array([-2.0, 3.0], np.float32), 0.25).tolist() == [-0.5, 3.0]
+
+
+def test_formats_structural_checks_on_host():
+    with pytest.raises(tg.ParameterError):
+        tg.Tcsc(4, 2, [0, 1], [0], [0, 0, 0], [])
+    with pytest.raises(tg.ParameterError):
+        tg.BlockedTcsc(4, 2, 2, np.zeros((1, 3)), [], np.zeros((2, 3)), [])
+    with pytest.raises(tg.ParameterError):
+        tg.InterleavedBlockedTcsc(4, 2, 4, 2, [], np.zeros(3))
+    with pytest.raises(tg.ParameterError):
+        tg.InterleavedBlockedTcsc(4, 2, 4, 2, [], np.zeros(7), symmetric_groups=True)
+    t = tg.InterleavedBlockedTcsc(4, 2, 4, 1, [0, 2, 3, 1], [0, 2, 3, 3, 3, 3, 4])
+    assert t.format_bytes() == 4 * (4 + 7) and t.num_blocks == 1 and t.nnz == 4
+    assert tg.format_bytes(t) == 44
+    with pytest.raises(tg.ParameterError):
+        tg.format_bytes(object())
+
+
+def _header_functions() -> list[str]:
+    src = open(os.path.join(ROOT, "include", "terngemm_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return re.findall(r"^\s*(?:int|size_t|const char\*)\s+(tg_\w+)\s*\(", src, flags=re.M)
+
+
+def test_c_abi_library_exports_every_declared_symbol():
+    names = _header_functions()
+    assert len(names) >= 20
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("library not built")
+    lib = ctypes.CDLL(_native.LIB_PATH)
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(_native.SIGNATURES), set(names) ^ set(_native.SIGNATURES)
+    L = _native.load()
+    assert L.tg_abi_version() == 1
+    # pure size queries need no device
+    assert L.tg_tiles_bytes(4096, 4096) == 32 * 4096 * 8 * 4
+    assert L.tg_build_workspace_bytes(4096, 4096, 4096) > 0
+    assert L.tg_gemm_workspace_bytes(256, 4096, 4096) >= 3 * 256 * 4096
+
+
+def test_compute_entry_points_fail_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(RuntimeError):
+        tg.tcsc_from_dense(np.zeros((2, 2), np.int8))
