@@ -45,8 +45,12 @@ class _Dual:
         return self._h
 
     def dev(self) -> torch.Tensor:
-        if self._d is None or not self._d.is_cuda:
+        if self._d is None:
             self._d = torch.from_numpy(np.ascontiguousarray(self._h)).to(_device(), non_blocking=False)
+        elif not self._d.is_cuda:
+            # host torch tensor: pinned memory uploads asynchronously on the current stream
+            src = self._d
+            self._d = src.to(_device(), non_blocking=src.is_pinned())
         return self._d
 
     def shape(self):

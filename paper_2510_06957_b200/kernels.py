@@ -248,7 +248,10 @@ class GemmRunner:
             r.a0, r.a1 = f.device("col_segment_ptr").data_ptr(), f.device("all_indices").data_ptr()
         return r
 
-    def launch(self, stream: int | None = None, ws: torch.Tensor | None = None) -> None:
+    def launch(self, stream: int | None = None, ws: torch.Tensor | None = None, stage: str = "all") -> None:
+        """Issue the call.  For the tensor-core path ``stage`` may be "prepare"
+        (X limb split) or "run" (tile MMA + exact-order fix-up) so a caller can
+        time the two halves separately; "all" issues both."""
         st = torch.cuda.current_stream().cuda_stream if stream is None else stream
         if ws is None:
             ws = self._ws if self._ws is not None else _workspace(self.ws_bytes, self.x.device, st)
@@ -256,8 +259,13 @@ class GemmRunner:
         M, K, N, ldx = self.M, self.K, self.N, self.ldx
         f = self.fmt
         if self.method == "mma":
-            nat.call("tg_gemm_tiles", x, M, K, ldx, _p(self.tiles), N, b, y, N, self.use_alpha, self.alpha,
-                     ctypes.byref(self.exact), _p(ws), ws.numel(), fl, st)
+            if stage in ("all", "prepare"):
+                nat.call("tg_gemm_tiles_prepare", x, M, K, ldx, _p(ws), ws.numel(), fl, st)
+            if stage in ("all", "run"):
+                nat.call("tg_gemm_tiles_run", x, M, K, ldx, _p(self.tiles), N, b, y, N, self.use_alpha, self.alpha,
+                         ctypes.byref(self.exact), _p(ws), ws.numel(), fl, st)
+            return
+        if stage == "prepare":
             return
         if self.kind in ("base", "unrolled"):
             nat.call("tg_gemm_tcsc", x, M, K, ldx, _p(f.device("col_start_pos")), _p(f.device("row_index_pos")),
