@@ -18,6 +18,8 @@ from .errors import CorruptionError, ParameterError
 
 LIB_NAME = "libterngemm_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# developer override (e.g. the clock64-instrumented libterngemm_b200_trace.so); never set in production
+LIB_PATH = os.environ.get("TG_LIB_PATH", LIB_PATH)
 
 TG_OK = 0
 TG_ERR_PARAM = 1

@@ -134,9 +134,8 @@ int tg_tiles_to_dense(const uint32_t* tiles, int64_t K, int64_t N, int8_t* W, vo
 
 // ------------------------------------------------------------------ GEMM (tiles)
 size_t tg_gemm_workspace_bytes(int64_t M, int64_t K, int64_t N) {
-  (void)N;
   if (M < 1 || K < 1) return 0;
-  const size_t a = xsplit_bytes(M, K);
+  const size_t a = mma_ws_bytes(M, K, N);
   const size_t b = gather_ws_bytes(M, K);
   return a > b ? a : b;
 }
@@ -166,21 +165,24 @@ int tg_gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, const u
     TG_REQUIRE(exact->B >= 1 && exact->g >= 1 && exact->uf >= 1 && exact->mr >= 1, TG_ERR_PARAM,
                "exact format: B, g, uf, mr must be >= 1");
   }
+  TG_REQUIRE(ws_bytes >= mma_ws_bytes(M, K, N), TG_ERR_PARAM, "workspace too small");
   TG_TRY(require_device());
-  cudaStream_t st = as_stream(stream);
-  TG_TRY(run_mma(M, K, tiles, N, bias, Y, ldy, use_alpha, alpha, ws, flags, st));
-  if (!exact) return TG_OK;
+  if (!exact) return run_mma(X, M, K, ldx, tiles, N, bias, Y, ldy, use_alpha, alpha, nullptr, ws, ws_bytes, flags,
+                             as_stream(stream));
   const int v = exact->variant;
+  MmaFixup fx{};
   const int64_t nb = (v == TG_VARIANT_BASE || v == TG_VARIANT_UNROLLED) ? 1 : ceil_div(K, exact->B);
-  const int64_t m_full = (v == TG_VARIANT_BLOCKED) ? M / exact->mr * exact->mr : 0;
-  const int uf = (v == TG_VARIANT_BASE) ? 1 : exact->uf;
-  if (v == TG_VARIANT_INTERLEAVED_BLOCKED || v == TG_VARIANT_VECTORIZED_OPTIMAL)
-    return run_fixup(v == TG_VARIANT_INTERLEAVED_BLOCKED ? GATHER_IB : GATHER_OPTIMAL, X, M, ldx,
-                     wide_rows(ws, M, K), exact->a0, exact->a1, nullptr, nullptr, nb, exact->g, 1, 0, N, bias, Y, ldy,
-                     use_alpha, alpha, flags, st);
-  const int gv = v == TG_VARIANT_BASE ? GATHER_BASE : v == TG_VARIANT_UNROLLED ? GATHER_UNROLLED : GATHER_BLOCKED;
-  return run_fixup(gv, X, M, ldx, wide_rows(ws, M, K), exact->a0, exact->a1, exact->a2, exact->a3, nb, 1, uf, m_full,
-                   N, bias, Y, ldy, use_alpha, alpha, flags, st);
+  fx.m_full = (v == TG_VARIANT_BLOCKED) ? M / exact->mr * exact->mr : 0;
+  if (v == TG_VARIANT_INTERLEAVED_BLOCKED || v == TG_VARIANT_VECTORIZED_OPTIMAL) {
+    fx.var = v == TG_VARIANT_INTERLEAVED_BLOCKED ? VAR_IB : VAR_OPTIMAL;
+    fx.args = GatherArgs{exact->a0, exact->a1, nullptr, nullptr, N, nb, fx.m_full, exact->g, 1};
+  } else {
+    fx.var = v == TG_VARIANT_BASE ? VAR_BASE : v == TG_VARIANT_UNROLLED ? VAR_UNROLLED : VAR_BLOCKED;
+    fx.args = GatherArgs{exact->a0, exact->a1, exact->a2, exact->a3, N, nb, fx.m_full, 1,
+                         v == TG_VARIANT_BASE ? 1 : exact->uf};
+  }
+  return run_mma(X, M, K, ldx, tiles, N, bias, Y, ldy, use_alpha, alpha, &fx, ws, ws_bytes, flags,
+                 as_stream(stream));
 }
 
 int tg_gemm_tiles(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N,

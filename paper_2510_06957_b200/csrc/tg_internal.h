@@ -17,13 +17,12 @@ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
 
 // tg_mma.cu
+struct GatherArgs;  // tg_walk.cuh
 int mma_pick_mt(int64_t M);
 size_t xsplit_bytes(int64_t M, int64_t K);
-const int32_t* wide_rows(void* ws, int64_t M, int64_t K);
+size_t mma_ws_bytes(int64_t M, int64_t K, int64_t N);
 int run_xsplit(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size_t ws_bytes, tg_device_flags* flags,
                cudaStream_t st);
-int run_mma(int64_t M, int64_t K, const uint32_t* tiles, int64_t N, const float* bias, float* Y, int64_t ldy,
-            int use_alpha, float alpha, void* ws, tg_device_flags* flags, cudaStream_t st);
 int run_pack_dense(const int8_t* W, int64_t K, int64_t N, int64_t ldw, uint32_t* tiles, tg_device_flags* flags,
                    cudaStream_t st);
 int run_pack_csc(const int32_t* col_start, const int32_t* rows, int64_t N, int64_t nblocks, bool neg,
@@ -41,9 +40,19 @@ int run_gather(int variant, const float* X, int64_t M, int64_t K, int64_t ldx, c
                const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, void* ws,
                tg_device_flags* flags, cudaStream_t st);
 
-int run_fixup(int variant, const float* X, int64_t M, int64_t ldx, const int32_t* rows, const int32_t* p0,
-              const int32_t* i0, const int32_t* p1, const int32_t* i1, int64_t nblocks, int g, int uf, int64_t m_full,
-              int64_t N, const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, tg_device_flags* flags,
-              cudaStream_t st);
 
+}  // namespace tg
+
+#include "tg_walk.cuh"
+
+namespace tg {
+// Exact-order recomputation of wide rows inside the tensor-core epilogue.
+struct MmaFixup {
+  int var;          // VAR_* of tg_walk.cuh
+  int64_t m_full;   // blocked: rows below take the banked order
+  GatherArgs args;
+};
+int run_mma(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N, const float* bias,
+            float* Y, int64_t ldy, int use_alpha, float alpha, const MmaFixup* fix, void* ws, size_t ws_bytes,
+            tg_device_flags* flags, cudaStream_t st);
 }  // namespace tg

@@ -7,133 +7,188 @@
 // then y <- (y > 0 ? y : alpha*y) in fp32 when PReLU is on (simd.py:410-417).
 //
 // Realisation (B200-native):
-//   1. tg_xsplit_kernel: each X row is scaled by a power of two 2^s so that
-//      max|x| < 2^22, rounded to an integer v, and v is split into three
-//      balanced signed base-256 digits (int8 "limbs").  Exact for integer X.
-//   2. tg_mma_kernel (warp specialised, one CTA per 128 n x MT m tile):
-//        warp 0   TMA: the three limb tiles of X -> smem (SWIZZLE_128B)
-//        warps 2-5 decode the 2-bit ternary tiles of W into int8 {-1,0,+1}
-//                 K-major SW128 smem tiles (the "expanded ternary tile")
-//        warp 1   one elected lane issues tcgen05.mma.kind::i8 with
-//                 A = W^T tile (M=128 rows = output columns n),
-//                 B = [limb0; limb1; limb2] (N = 3*MT rows = output rows m)
-//                 into an int32 accumulator in TMEM.  Integer accumulation is
-//                 exact, so the result does not depend on summation order.
-//        warps 2-5 epilogue: tcgen05.ld the three limb sums, recombine
-//                 exactly in int64, scale by 2^-s in fp64, add the bias,
-//                 round once to fp32, PReLU, coalesced store of Y.
+//   1. tg_xsplit_kernel: each X row is staged once in shared memory, scaled by
+//      a power of two 2^s so that max|x| < 2^22, rounded to an integer v, and v
+//      is split into three balanced signed base-256 digits (int8 "limbs").
+//      Exact for integer X.
+//   2. tg_mma_kernel: persistent, warp-specialised, one CTA per SM.  A work
+//      unit is (128 output columns) x (MT output rows) x (a K range):
+//        warp 0    TMA: the three limb tiles of X (SWIZZLE_128B) and the
+//                  packed 2-bit ternary tile of W (one 4 KB bulk copy) per stage
+//        warps 2-5 decode the packed tile in shared memory into int8 {-1,0,+1}
+//                  K-major SW128 tiles (the "expanded ternary tile")
+//        warp 1    one elected lane issues tcgen05.mma.kind::i8 with
+//                  A = W^T tile (M=128 rows = output columns n),
+//                  B = [limb0; limb1; limb2] (N = 3*MT rows = output rows m)
+//                  into one of two int32 TMEM accumulators (double-buffered so
+//                  the epilogue of a unit overlaps the MMAs of the next).
+//                  Integer accumulation is exact: the result does not depend
+//                  on summation order, so K may be split across CTAs.
+//        warps 6-9 epilogue: tcgen05.ld the three limb sums, recombine exactly
+//                  in int64, scale by 2^-s in fp64, add the bias, round once to
+//                  fp32, PReLU, coalesced store of Y.  Split-K units write
+//                  int64 partials; the last unit of a tile reduces them.
+//                  Rows flagged "wide" by the split (negative scale) are then recomputed in the
+//                  reference's exact operation order (tg_walk.cuh).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <cstdint>
+#include <cstdlib>
 
 #include "tg_ptx.cuh"
 #include "tg_internal.h"
+#include "tg_walk.cuh"
 
 namespace tg {
 
 // ------------------------------------------------------------------ X split
-// One CTA per (padded) row.  limbs: [3][M_pad][K_pad] int8, rscale: [M_pad] f64,
-// wide: [1 + M_pad] int32 (count, then row ids).
+// One CTA per (padded) row.  limbs: [3][M_pad][K_pad] int8, rscale: [M_pad] f64.
 //
 // Row m is scaled by 2^s, s = 22 - e with amax < 2^e, so |x 2^s| < 2^22; the
 // rounded integer v splits into balanced base-256 digits v = d0 2^16 + d1 2^8 + d2.
 // The grid step 2^(e-22) is relative to the row maximum, so a row whose nonzero
 // entries span a wide dynamic range (amax > kWideRatio * rms of its nonzeros)
-// is listed in `wide` and later recomputed by the exact-order fix-up kernel;
-// its rscale is stored negated so the MMA epilogue leaves its PReLU count alone.
+// gets its rscale stored negated: the MMA epilogue then recomputes the row in
+// the exact reference order (and takes its PReLU count there).
 constexpr float kWideRatio = 16.f;
+constexpr int64_t XS_SMEM_MAX_K = 16384;  // rows up to 64 KB are staged in shared memory
 
-__global__ void __launch_bounds__(256) tg_xsplit_kernel(const float* __restrict__ X, int64_t M, int64_t K,
-                                                        int64_t ldx, int8_t* __restrict__ limbs,
-                                                        double* __restrict__ rscale, int32_t* __restrict__ wide,
-                                                        int64_t M_pad, int64_t K_pad,
-                                                        tg_device_flags* __restrict__ flags) {
-  const int64_t m = blockIdx.x;
-  const float* row = X + m * ldx;
-  __shared__ float red[8];
-  __shared__ float red2[8];
-  __shared__ int redn[8];
-  float amax = 0.f;
-  if (m < M) {
-    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) amax = fmaxf(amax, fabsf(row[k]));
-  }
-  for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = amax;
+template <int XS_THREADS>
+__device__ __forceinline__ float block_max(float v, float* red) {
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
   __syncthreads();
-  amax = red[0];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  v = red[0];
 #pragma unroll
-  for (int i = 1; i < 8; ++i) amax = fmaxf(amax, red[i]);
-  const bool finite = amax <= 3.402823466e38f;  // false for inf / nan
-  int s = 0;
-  if (m < M && amax > 0.f) {
-    if (!finite) {
-      if (threadIdx.x == 0 && flags) atomicOr(&flags->bad_input, 4);
+  for (int i = 1; i < XS_THREADS / 32; ++i) v = fmaxf(v, red[i]);
+  return v;
+}
+template <int XS_THREADS>
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  v = 0.f;
+#pragma unroll
+  for (int i = 0; i < XS_THREADS / 32; ++i) v += red[i];
+  return v;
+}
+
+__device__ __forceinline__ uint32_t limb_digits(int v, uint32_t& p1, uint32_t& p2, int j) {
+  const int d2 = ((v + 128) & 255) - 128;
+  const int v1 = (v - d2) >> 8;
+  const int d1 = ((v1 + 128) & 255) - 128;
+  const int d0 = (v1 - d1) >> 8;
+  p1 |= (uint32_t(d1) & 255u) << (8 * j);
+  p2 |= (uint32_t(d2) & 255u) << (8 * j);
+  return (uint32_t(d0) & 255u) << (8 * j);
+}
+
+// SMEM: the row is loaded once into dynamic shared memory (K_pad floats);
+// otherwise every pass re-reads it from global memory (L2-resident).
+template <bool SMEM, int XS_THREADS>
+__global__ void __launch_bounds__(XS_THREADS) tg_xsplit_kernel(const float* __restrict__ X, int64_t M, int64_t K,
+                                                               int64_t ldx, int8_t* __restrict__ limbs,
+                                                               double* __restrict__ rscale,
+                                                               int64_t M_pad,
+                                                               int64_t K_pad, tg_device_flags* __restrict__ flags) {
+  extern __shared__ float srow[];
+  __shared__ float red[XS_THREADS / 32];
+  grid_dep_launch();  // the MMA kernel may start its prologue (it waits before reading our output)
+  const int64_t m = blockIdx.x;
+  const float* grow = X + m * ldx;
+  const bool in = m < M;
+  // pass 1: stage the row, amax
+  float amax = 0.f;
+  if (in) {
+    if (SMEM) {
+      const bool vec = ((ldx & 3) == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+      if (vec) {
+        const int64_t K4 = K >> 2;
+        for (int64_t i = threadIdx.x; i < K4; i += XS_THREADS) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(grow) + i);
+          reinterpret_cast<float4*>(srow)[i] = v;
+          amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        }
+        for (int64_t k = (K4 << 2) + threadIdx.x; k < K; k += XS_THREADS) {
+          const float v = __ldg(grow + k);
+          srow[k] = v;
+          amax = fmaxf(amax, fabsf(v));
+        }
+      } else {
+        for (int64_t k = threadIdx.x; k < K; k += XS_THREADS) {
+          const float v = __ldg(grow + k);
+          srow[k] = v;
+          amax = fmaxf(amax, fabsf(v));
+        }
+      }
     } else {
-      int e;
-      frexpf(amax, &e);  // amax < 2^e
-      s = 22 - e;        // |x * 2^s| < 2^22
+      for (int64_t k = threadIdx.x; k < K; k += XS_THREADS) amax = fmaxf(amax, fabsf(__ldg(grow + k)));
     }
   }
-  // dynamic range of the nonzero entries: sum (x / amax)^2 and their count
-  bool is_wide = false;
-  if (m < M && amax > 0.f && finite) {
-    const float inv = 1.f / amax;
-    float s2 = 0.f;
-    int nz = 0;
-    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
-      const float t = row[k] * inv;
-      s2 += t * t;
-      nz += t != 0.f;
-    }
-    for (int o = 16; o; o >>= 1) {
-      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-      nz += __shfl_xor_sync(0xffffffffu, nz, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-      red2[threadIdx.x >> 5] = s2;
-      redn[threadIdx.x >> 5] = nz;
-    }
-    __syncthreads();
-    s2 = 0.f;
-    nz = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      s2 += red2[i];
-      nz += redn[i];
-    }
-    is_wide = float(nz) > kWideRatio * kWideRatio * s2;  // amax / rms(nonzeros) > kWideRatio
+  amax = block_max<XS_THREADS>(amax, red);  // (also orders the smem stores before pass 2)
+  const bool finite = amax <= 3.402823466e38f;  // false for inf / nan
+  const bool live = in && amax > 0.f && finite;
+  int s = 0;
+  if (live) {
+    int e;
+    frexpf(amax, &e);  // amax < 2^e
+    s = 22 - e;        // |x * 2^s| < 2^22
+  } else if (in && !finite && threadIdx.x == 0 && flags) {
+    atomicOr(&flags->bad_input, 4);
   }
-  if (threadIdx.x == 0) {
-    const double sc = (m < M && amax > 0.f && finite) ? ldexp(1.0, -s) : 0.0;
-    rscale[m] = is_wide ? -sc : sc;
-    if (is_wide && wide) {
-      const int slot = atomicAdd(wide, 1);
-      wide[1 + slot] = int32_t(m);
-    }
-  }
+  // pass 2: limbs (16 consecutive k per thread-iteration) + dynamic range statistics.
+  // x * 2^s as two exact power-of-two multiplies (2^s alone may exceed the float range).
+  const int s_a = s > 126 ? 126 : (s < -126 ? -126 : s);
+  const float sc_a = __int_as_float((127 + s_a) << 23), sc_b = __int_as_float((127 + s - s_a) << 23);
+  const float inv = live ? 1.f / amax : 0.f;
+  float s2 = 0.f, nzf = 0.f;
   int8_t* l0 = limbs + m * K_pad;
   int8_t* l1 = limbs + (M_pad + m) * K_pad;
   int8_t* l2 = limbs + (2 * M_pad + m) * K_pad;
-  const bool live = m < M && amax > 0.f && finite;
-  for (int64_t k0 = int64_t(threadIdx.x) * 4; k0 < K_pad; k0 += int64_t(blockDim.x) * 4) {
-    uint32_t p0 = 0, p1 = 0, p2 = 0;
+  constexpr int WORDS = XS_THREADS >= 1024 ? 1 : 4;  // 4-byte words of each limb per thread-iteration
+  constexpr int VEC = 4 * WORDS;
+  for (int64_t k0 = int64_t(threadIdx.x) * VEC; k0 < K_pad; k0 += int64_t(XS_THREADS) * VEC) {
+    uint32_t q0[WORDS], q1[WORDS], q2[WORDS];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t k = k0 + j;
-      int v = 0;
-      if (live && k < K) v = __float2int_rn(ldexpf(row[k], s));
-      const int d2 = ((v + 128) & 255) - 128;
-      const int v1 = (v - d2) >> 8;
-      const int d1 = ((v1 + 128) & 255) - 128;
-      const int d0 = (v1 - d1) >> 8;
-      p0 |= (uint32_t(d0) & 255u) << (8 * j);
-      p1 |= (uint32_t(d1) & 255u) << (8 * j);
-      p2 |= (uint32_t(d2) & 255u) << (8 * j);
+    for (int w = 0; w < WORDS; ++w) {
+      uint32_t p0 = 0, p1 = 0, p2 = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t k = k0 + 4 * w + j;
+        int v = 0;
+        if (live && k < K) {
+          const float x = SMEM ? srow[k] : __ldg(grow + k);
+          v = __float2int_rn((x * sc_a) * sc_b);
+          const float t = x * inv;
+          s2 += t * t;
+          nzf += (x != 0.f) ? 1.f : 0.f;
+        }
+        p0 |= limb_digits(v, p1, p2, j);
+      }
+      q0[w] = p0;
+      q1[w] = p1;
+      q2[w] = p2;
     }
-    *reinterpret_cast<uint32_t*>(l0 + k0) = p0;
-    *reinterpret_cast<uint32_t*>(l1 + k0) = p1;
-    *reinterpret_cast<uint32_t*>(l2 + k0) = p2;
+    if constexpr (WORDS == 4) {
+      *reinterpret_cast<uint4*>(l0 + k0) = make_uint4(q0[0], q0[1], q0[2], q0[3]);
+      *reinterpret_cast<uint4*>(l1 + k0) = make_uint4(q1[0], q1[1], q1[2], q1[3]);
+      *reinterpret_cast<uint4*>(l2 + k0) = make_uint4(q2[0], q2[1], q2[2], q2[3]);
+    } else {
+      *reinterpret_cast<uint32_t*>(l0 + k0) = q0[0];
+      *reinterpret_cast<uint32_t*>(l1 + k0) = q1[0];
+      *reinterpret_cast<uint32_t*>(l2 + k0) = q2[0];
+    }
+  }
+  s2 = block_sum<XS_THREADS>(s2, red);
+  nzf = block_sum<XS_THREADS>(nzf, red);
+  if (threadIdx.x == 0) {
+    const bool is_wide = live && nzf > kWideRatio * kWideRatio * s2;  // amax / rms(nonzeros) > kWideRatio
+    const double sc = live ? ldexp(1.0, -s) : 0.0;
+    rscale[m] = is_wide ? -sc : sc;
   }
 }
 
@@ -155,172 +210,510 @@ __device__ __forceinline__ uint4 decode_word(uint32_t w) {
   return o;
 }
 
+// ------------------------------------------------------------------ trace (debug builds only)
+#ifdef TG_TRACE
+// [cta slot][event][iteration]: clock64 stamps of CTA 0 and CTA 1, first 512 pipeline iterations
+__device__ unsigned long long g_tg_trace[2][8][512];
+#define TG_STAMP(ev, it)                                                           \
+  do {                                                                             \
+    if (blockIdx.x < 2 && (it) < 512) g_tg_trace[blockIdx.x][ev][it] = clock64(); \
+  } while (0)
+#else
+#define TG_STAMP(ev, it) \
+  do {                   \
+  } while (0)
+#endif
+
 // ------------------------------------------------------------------ MMA
-template <int MT, int STAGES>
-struct MmaCfg {
-  static constexpr int BN = 128;                 // output columns per CTA (= MMA M)
-  static constexpr int BK = 128;                 // k per stage (bytes, int8)
-  static constexpr int NMMA = 3 * MT;            // MMA N: three limbs of MT rows
-  static constexpr int A_BYTES = BN * BK;        // decoded W^T stage
-  static constexpr int B_BYTES = NMMA * BK;      // X limb stage
-  static constexpr int TMEM_COLS = NMMA <= 32 ? 32 : NMMA <= 64 ? 64 : NMMA <= 128 ? 128 : 256;
-  static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
-  static_assert(MT % 16 == 0 && NMMA <= 256, "bad MT");
+struct MmaParams {
+  const uint32_t* tiles;   // [KC][N_pad][8] packed ternary words
+  const double* rscale;    // [M_pad], < 0 marks a wide row
+  const float* bias;       // [N] or null
+  float* Y;
+  int64_t ldy;
+  int M, N, KC, KS, M_pad, N_pad, MB, NB, splits;  // KC 128-k chunks, KS = ceil(KC/2) stages
+  int NBG;                 // column-block groups: one group of CS blocks per cluster unit
+  int units;               // cluster units = MB * NBG * splits
+  int use_alpha;
+  float alpha;
+  long long* part;         // split-K partials [splits][M_pad][N_pad] (splits > 1)
+  int32_t* counters;       // [MB * NB] arrival counters, zero between launches
+  tg_device_flags* flags;
+  int fix_var;             // < 0: no exact-order fix-up of wide rows
+  int64_t m_full;          // blocked: rows < m_full take the banked order
+  GatherArgs fix;
+  const float* X;          // original X (fix-up reads it in place)
+  int64_t ldx;
 };
 
-template <int MT, int STAGES>
-__global__ void __launch_bounds__(192, 1)
-    tg_mma_kernel(const __grid_constant__ CUtensorMap xmap, const uint32_t* __restrict__ tiles,
-                  const double* __restrict__ rscale, const float* __restrict__ bias, float* __restrict__ Y,
-                  int64_t ldy, int M, int N, int KC, int M_pad, int N_pad, int use_alpha, float alpha,
-                  tg_device_flags* __restrict__ flags) {
-  using C = MmaCfg<MT, STAGES>;
+// Tile configuration.  A pipeline stage covers 256 k (two 128-k chunks: 8
+// MMAs of K = 32 and ONE tcgen05.commit -- a commit costs about as much as an
+// MMA, so 4-MMA stages ran at ~55% of the issue rate, scratch/mma_bench.cu).
+// TMEM (512 columns x 128 lanes x 32 bit) holds ACC_BUFS accumulators of NMMA
+// int32 columns plus two 64-column slots of the decoded W^T tile (128 lanes x
+// 256 int8): the expanded ternary tile never touches shared memory, which
+// carries only the X limbs and the packed W.
+template <int MT>
+struct MmaCfg {
+  static constexpr int BN = 128;                 // output columns per unit (= MMA M)
+  static constexpr int BK = 128;                 // k per chunk (bytes, int8; one 128-byte swizzle atom)
+  static constexpr int CH = 2;                   // chunks per stage
+  static constexpr int NMMA = 3 * MT;            // MMA N: three limbs of MT rows
+  static constexpr int B_CHUNK = NMMA * BK;      // X limbs of one chunk
+  static constexpr int B_BYTES = CH * B_CHUNK;
+  static constexpr int P_CHUNK = BN * 32;        // packed 2-bit W of one chunk (128 k x 128 n)
+  static constexpr int P_BYTES = CH * P_CHUNK;
+#ifndef TG_SMEM_BUDGET
+#define TG_SMEM_BUDGET 226000
+#endif
+  // packed-W ring: deep (HBM latency), released by the decoders as soon as they read it
+  static constexpr int P_STAGES = 6;
+  // X-limb ring: released by the MMA commit
+  static constexpr int STAGES_RAW = (TG_SMEM_BUDGET - 3072 - P_STAGES * P_BYTES) / B_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int ACC_COLS = (NMMA + 31) / 32 * 32;
+  static constexpr int A_SLOTS = 2;
+  static constexpr int A_COLS = CH * 32;         // TMEM columns of one decoded stage
+  static constexpr int ACC_BUFS = (2 * ACC_COLS + A_SLOTS * A_COLS <= 512) ? 2 : 1;
+  static constexpr int A_BASE = ACC_BUFS * ACC_COLS;  // first TMEM column of the A ring
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int SMEM = STAGES * B_BYTES + P_STAGES * P_BYTES + 1024 /*align*/ + 2048 /*barriers, scales*/;
+  static constexpr int EPI_WARP0 = 7;            // warps: 0 X producer, 1 MMA, 2-5 decoders, 6 W producer
+  static constexpr int EPI_WARPS = 8;            // two per TMEM lane quarter, splitting the rows
+  static constexpr int THREADS = 32 * (EPI_WARP0 + EPI_WARPS);
+  static_assert(MT % 16 == 0 && NMMA <= 256, "bad MT");
+  static_assert(STAGES >= A_SLOTS, "slot release rides on the stage barrier: needs STAGES >= A_SLOTS");
+  static_assert(A_BASE + A_SLOTS * A_COLS <= 512, "TMEM budget");
+};
+
+// Cluster unit u -> this CTA's column block nb (may be >= NB: a "ghost" block that
+// only helps its cluster load the shared X tile), row block mb and stage range.
+template <int CS>
+__device__ __forceinline__ void unit_coords(const MmaParams& p, int u, int crank, int& nb, int& mb, int& ks0, int& ks1,
+                                            int& split) {
+  nb = (u % p.NBG) * CS + crank;
+  const int rest = u / p.NBG;
+  split = rest % p.splits;
+  mb = rest / p.splits;
+  ks0 = int((int64_t(split) * p.KS) / p.splits);
+  ks1 = int((int64_t(split + 1) * p.KS) / p.splits);
+}
+
+__device__ __forceinline__ float finish(long long tot, double rs, double bn, int use_alpha, float alpha,
+                                        bool count_it, unsigned long long& npos, bool& bad) {
+  const double v = static_cast<double>(tot) * fabs(rs) + bn;
+  float y = static_cast<float>(v);
+  if (use_alpha && !(y > 0.f)) {
+    y = alpha * y;
+    npos += count_it;
+  }
+  bad |= !isfinite(y);
+  return y;
+}
+
+// Finish 16 consecutive rows of one output column: y = fp32(tot * |rs| + b)
+// (tot * |rs| is exact: rs is a power of two), PReLU, store.  Straight-line
+// so the 16 conversions pipeline; rows >= M are not stored.
+__device__ __forceinline__ void emit16(const long long (&tot)[16], uint32_t rs_addr, double bn, const MmaParams& p,
+                                       int m_first, bool n_ok, float* yrow, unsigned long long& npos, bool& bad) {
+  double rs[16];
+#pragma unroll
+  for (int j = 0; j < 16; j += 2) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(rs[j]), "=d"(rs[j + 1]) : "r"(rs_addr + 8u * j));
+  }
+  float y[16];
+  unsigned cnt = 0;
+  float mx = 0.f;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+#ifdef TG_EPI_FAST
+    float v = __fmaf_rn(static_cast<float>(tot[j]), static_cast<float>(fabs(rs[j])), static_cast<float>(bn));
+#else
+    float v = static_cast<float>(fma(static_cast<double>(tot[j]), fabs(rs[j]), bn));
+#endif
+    const bool neg = p.use_alpha && !(v > 0.f);
+    const bool live = n_ok && (m_first + j) < p.M;
+    cnt += (neg && live && (rs[j] >= 0.0 || p.fix_var < 0)) ? 1u : 0u;
+    y[j] = neg ? p.alpha * v : v;
+    mx = fmaxf(mx, live ? fabsf(y[j]) : 0.f);
+  }
+  bad |= !(mx <= 3.402823466e38f);
+  if (!n_ok) return;
+  npos += cnt;
+#ifdef TG_EPI_NOSTORE
+  if (y[0] == 123.f && y[15] == 7.f) yrow[0] = y[3];
+  return;
+#endif
+  if (m_first + 16 <= p.M) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) yrow[int64_t(j) * p.ldy] = y[j];
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (m_first + j < p.M) yrow[int64_t(j) * p.ldy] = y[j];
+  }
+}
+
+template <int MT, int CS>
+__global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
+    tg_mma_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ MmaParams p) {
+  using C = MmaCfg<MT>;
+  static_assert(CS == 1 || CS == 2 || CS == 4, "cluster size");
+  static_assert(MT / CS >= 8, "multicast slices must be whole 8-row swizzle atoms");
+  constexpr int SL = MT / CS;                       // X-limb rows this CTA loads and multicasts
+  constexpr uint16_t CMASK = uint16_t((1u << CS) - 1u);
+  constexpr int S = C::STAGES;
+  constexpr int AS = C::A_SLOTS;
+  constexpr int NACC = C::ACC_BUFS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * C::A_BYTES;
-  uint64_t* full_a = reinterpret_cast<uint64_t*>(sB + STAGES * C::B_BYTES);
-  uint64_t* full_b = full_a + STAGES;
-  uint64_t* empty = full_b + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  constexpr int SP = C::P_STAGES;
+  uint8_t* sB = smem;                       // S x B_BYTES (multiples of 1024)
+  uint8_t* sP = sB + S * C::B_BYTES;        // SP x P_BYTES
+  uint64_t* full_raw = reinterpret_cast<uint64_t*>(sP + SP * C::P_BYTES);  // [S] X limbs landed
+  uint64_t* empty = full_raw + S;           // [S]  MMAs of the stage done (all cluster CTAs)
+  uint64_t* p_full = empty + S;             // [SP] packed W landed
+  uint64_t* p_empty = p_full + SP;          // [SP] decoders done reading it
+  uint64_t* a_full = p_empty + SP;          // [AS] decoded W^T slot written
+  uint64_t* tfull = a_full + AS;            // [2]
+  uint64_t* tempty = tfull + 2;             // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int32_t* last_flag = reinterpret_cast<int32_t*>(tmem_slot + 1);
+  // [80] row scales of the current unit (16-byte aligned for ld.shared.v2.f64), then [4] wide-row masks
+  double* rs_s = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(tmem_slot + 2) + 15) & ~uintptr_t(15));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * C::BN;
-  const int m0 = blockIdx.y * MT;
+  const int crank = CS > 1 ? int(cluster_ctarank()) : 0;
+  const int cid = int(blockIdx.x) / CS, ncl = int(gridDim.x) / CS;
+  if (threadIdx.x == 0) TG_STAMP(7, 0);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full_a[s], 4);
-      mbar_init(&full_b[s], 1);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_raw[s], 1);
+      mbar_init(&empty[s], CS);  // every CTA of the cluster must be done with the shared X stage
     }
-    mbar_init(tmem_full, 1);
+    for (int s = 0; s < SP; ++s) {
+      mbar_init(&p_full[s], 1);
+      mbar_init(&p_empty[s], 4);
+    }
+    for (int s = 0; s < AS; ++s) mbar_init(&a_full[s], 4);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], C::EPI_WARPS);
+    }
     fence_mbar_init();
     tma_prefetch_desc(&xmap);
   }
   if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  if (CS > 1) cluster_sync_all();  // peers multicast into our smem / arrive on our barriers
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) TG_STAMP(7, 1);
+  // Programmatic dependent launch: everything above overlapped the X split; its
+  // limbs and row scales are read below this point.
+  grid_dep_wait();
 
   if (warp == 0) {
-    // ---------------- TMA producer: X limbs
+    // ---------------- producer of the X limbs (TMA 2D, multicast to the cluster)
     if (lane == 0) {
-      for (int kc = 0; kc < KC; ++kc) {
-        const int s = kc % STAGES;
-        const uint32_t round = kc / STAGES;
-        mbar_wait(&empty[s], (round & 1) ^ 1);
-        mbar_arrive_expect_tx(&full_b[s], C::B_BYTES);
-        uint8_t* dst = sB + s * C::B_BYTES;
+      uint32_t it = 0;
+      for (int u = cid; u < p.units; u += ncl) {
+        int nb, mb, ks0, ks1, split;
+        unit_coords<CS>(p, u, crank, nb, mb, ks0, ks1, split);
+        const int m0 = mb * MT;
+        for (int ks = ks0; ks < ks1; ++ks, ++it) {
+          const int s = int(it % S);
+          const uint32_t r = it / S;
+          const int nch = (2 * ks + 1 < p.KC) ? 2 : 1;
+          mbar_wait(&empty[s], (r & 1) ^ 1);
+          TG_STAMP(0, it);
+          mbar_arrive_expect_tx(&full_raw[s], uint32_t(nch * C::B_CHUNK));
+          for (int c = 0; c < nch; ++c) {
+            const int kc = 2 * ks + c;
+            uint8_t* dst = sB + s * C::B_BYTES + c * C::B_CHUNK;
 #pragma unroll
-        for (int l = 0; l < 3; ++l)
-          tma_load_2d(dst + l * MT * C::BK, &xmap, &full_b[s], kc * C::BK, l * M_pad + m0);
+            for (int l = 0; l < 3; ++l) {
+              uint8_t* d = dst + (l * MT + crank * SL) * C::BK;
+              const int row = l * p.M_pad + m0 + crank * SL;
+              if (CS == 1) tma_load_2d(d, &xmap, &full_raw[s], kc * C::BK, row);
+              else tma_load_2d_mc(d, &xmap, &full_raw[s], kc * C::BK, row, CMASK);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 6) {
+    // ---------------- producer of the packed W tiles (own ring, runs ahead of the X ring)
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int u = cid; u < p.units; u += ncl) {
+        int nb, mb, ks0, ks1, split;
+        unit_coords<CS>(p, u, crank, nb, mb, ks0, ks1, split);
+        const int nsrc = nb < p.NB ? nb * C::BN : (p.NB - 1) * C::BN;  // ghost blocks decode a valid tile
+        for (int ks = ks0; ks < ks1; ++ks, ++it) {
+          const int sp = int(it % SP);
+          const uint32_t rp = it / SP;
+          const int nch = (2 * ks + 1 < p.KC) ? 2 : 1;
+          mbar_wait(&p_empty[sp], (rp & 1) ^ 1);
+          mbar_arrive_expect_tx(&p_full[sp], uint32_t(nch * C::P_CHUNK));
+          for (int c = 0; c < nch; ++c)
+            bulk_load(sP + sp * C::P_BYTES + c * C::P_CHUNK, p.tiles + (size_t(2 * ks + c) * p.N_pad + nsrc) * 8,
+                      C::P_CHUNK, &p_full[sp]);
+        }
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer
+    // ---------------- MMA issuer: A = decoded W^T from TMEM, B = X limbs from smem.
+    // One commit per stage (to the stage's `empty` barrier, in every cluster CTA);
+    // the decoders derive the release of the A slot from the same barrier.
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_i8(128, C::NMMA);
-      for (int kc = 0; kc < KC; ++kc) {
-        const int s = kc % STAGES;
-        const uint32_t round = kc / STAGES;
-        mbar_wait(&full_a[s], round & 1);
-        mbar_wait(&full_b[s], round & 1);
+      uint32_t it = 0, lu = 0;
+      for (int u = cid; u < p.units; u += ncl, ++lu) {
+        int nb, mb, ks0, ks1, split;
+        unit_coords<CS>(p, u, crank, nb, mb, ks0, ks1, split);
+        const uint32_t acc = lu % NACC, use = lu / NACC;
+        mbar_wait(&tempty[acc], (use & 1) ^ 1);
         tc_fence_after();
-        const uint64_t da = smem_desc_k_sw128(smem_u32(sA + s * C::A_BYTES));
-        const uint64_t db = smem_desc_k_sw128(smem_u32(sB + s * C::B_BYTES));
+        const uint32_t dtm = tmem_base + acc * C::ACC_COLS;
+        for (int ks = ks0; ks < ks1; ++ks, ++it) {
+          const int s = int(it % S);
+          const int a = int(it % AS);
+          const uint32_t ra = it / AS;
+          const int nch = (2 * ks + 1 < p.KC) ? 2 : 1;
+          // a_full implies full_raw: the decoders arrive on a_full only after they
+          // observed this stage's bytes land, and the MMA reads the X limbs through
+          // the same async proxy that wrote them.
+          TG_STAMP(1, it);
+          mbar_wait(&a_full[a], ra & 1);
+          TG_STAMP(2, it);
+          tc_fence_after();
+          const uint64_t db = smem_desc_k_sw128(smem_u32(sB + s * C::B_BYTES));
+          const uint32_t ta = tmem_base + uint32_t(C::A_BASE + a * C::A_COLS);
+          for (int c = 0; c < nch; ++c) {
 #pragma unroll
-        for (int kk = 0; kk < C::BK / 32; ++kk) {
-          // +32 bytes along K inside the 128-byte swizzle atom = +2 in the (>>4) address field
-          mma_i8(tmem_base, da + uint64_t(kk * 2), db + uint64_t(kk * 2), idesc, (kc | kk) != 0);
+            for (int kk = 0; kk < C::BK / 32; ++kk) {
+              // K step of 32 int8: +8 TMEM columns for A, +32 bytes (= +2 in the >>4 field) for B
+              mma_i8_tmem_a(dtm, ta + uint32_t(c * 32 + kk * 8),
+                            db + uint64_t((c * C::B_CHUNK) >> 4) + uint64_t(kk * 2), idesc,
+                            (ks != ks0 || c != 0 || kk != 0) ? 1u : 0u);
+            }
+          }
+          if (CS == 1) mma_commit(&empty[s]);
+          else mma_commit_mc(&empty[s], CMASK);
+          TG_STAMP(3, it);
         }
-        mma_commit(&empty[s]);
+        mma_commit(&tfull[acc]);
       }
-      mma_commit(tmem_full);
+    }
+  } else if (warp < 6) {
+    // ---------------- decoders (warps 2..5): packed smem -> decoded W^T rows in TMEM.
+    // Warp w may only access TMEM lanes 32*(w%4)..+31; lane = W^T row = output column.
+    const int q = warp & 3;
+    const uint32_t row = uint32_t(q * 32 + lane);
+    const uint32_t lane_addr = uint32_t(q * 32) << 16;
+    uint32_t it = 0;
+    for (int u = cid; u < p.units; u += ncl) {
+      int nb, mb, ks0, ks1, split;
+      unit_coords<CS>(p, u, crank, nb, mb, ks0, ks1, split);
+      for (int ks = ks0; ks < ks1; ++ks, ++it) {
+        const int s = int(it % S);
+        const uint32_t r = it / S;
+        const int a = int(it % AS);
+        const int nch = (2 * ks + 1 < p.KC) ? 2 : 1;
+        const int sp = int(it % SP);
+        mbar_wait(&p_full[sp], (it / SP) & 1);
+        if (q == 0 && lane == 0) TG_STAMP(4, it);
+        uint4 w[2][2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          if (c < nch) {
+            const uint32_t src = smem_u32(sP + sp * C::P_BYTES + c * C::P_CHUNK) + row * 32u;
+            w[c][0] = lds128(src);
+            w[c][1] = lds128(src + 16u);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_empty[sp]);  // packed tile consumed (values are in registers)
+        // slot a was last read by the MMAs of iteration it - AS, released with stage
+        // (it - AS) % S (at most one phase behind: STAGES >= A_SLOTS)
+        if (it >= uint32_t(AS)) {
+          const uint32_t prev = it - AS;
+          mbar_wait(&empty[prev % S], (prev / S) & 1);
+        }
+        if (q == 0 && lane == 0) TG_STAMP(5, it);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          if (c < nch) {
+            uint32_t v[32];
+            const uint32_t pw[8] = {w[c][0].x, w[c][0].y, w[c][0].z, w[c][0].w,
+                                    w[c][1].x, w[c][1].y, w[c][1].z, w[c][1].w};
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint4 o = decode_word(pw[j]);
+              v[4 * j + 0] = o.x;
+              v[4 * j + 1] = o.y;
+              v[4 * j + 2] = o.z;
+              v[4 * j + 3] = o.w;
+            }
+            tmem_st32(tmem_base + lane_addr + uint32_t(C::A_BASE + a * C::A_COLS + c * 32), v);
+          }
+        }
+        tmem_st_wait();
+        // the MMA waits only on a_full: make it imply that this stage's X limbs landed too
+        mbar_wait(&full_raw[s], r & 1);
+        if (q == 0 && lane == 0) TG_STAMP(6, it);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_full[a]);
+      }
     }
   } else {
-    // ---------------- decoders (warps 2..5), then epilogue
-    const int t = threadIdx.x - 64;  // 0..127 = row of the W^T tile
-    const uint4* src = reinterpret_cast<const uint4*>(tiles) + (size_t(n0 + t) * 2);
-    const size_t kc_stride = size_t(N_pad) * 2;  // uint4 per kc
-    uint4 c0 = __ldg(src), c1 = __ldg(src + 1);
-    const uint32_t row_off = uint32_t(t) * 128u;
-    const uint32_t sw = uint32_t(t) & 7u;
-    for (int kc = 0; kc < KC; ++kc) {
-      const int s = kc % STAGES;
-      const uint32_t round = kc / STAGES;
-      uint4 n0v = make_uint4(0, 0, 0, 0), n1v = make_uint4(0, 0, 0, 0);
-      if (kc + 1 < KC) {
-        n0v = __ldg(src + (kc + 1) * kc_stride);
-        n1v = __ldg(src + (kc + 1) * kc_stride + 1);
-      }
-      mbar_wait(&empty[s], (round & 1) ^ 1);
-      uint8_t* a = sA + s * C::A_BYTES + row_off;
-      const uint32_t w[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        *reinterpret_cast<uint4*>(a + ((uint32_t(c) ^ sw) << 4)) = decode_word(w[c]);
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&full_a[s]);
-      c0 = n0v;
-      c1 = n1v;
-    }
-
-    // ---------------- epilogue
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int n = n0 + q * 32 + lane;
-    const bool n_ok = n < N;
-    const double bn = (n_ok && bias) ? double(bias[n]) : 0.0;
+    // ---------------- epilogue (warps 7..14): warp w owns TMEM lane quarter w%4
+    // (32 output columns) and the 16-row chunks of parity `half`.
+    constexpr int ET = 32 * C::EPI_WARPS;
+    const int q = warp & 3;
+    const int et = threadIdx.x - 32 * C::EPI_WARP0;  // 0..ET-1
+    const int half = (warp - C::EPI_WARP0) >> 2;
+    const uint32_t rs_addr = smem_u32(rs_s);
+    uint32_t* wmask = reinterpret_cast<uint32_t*>(rs_s + 80);  // [4] wide-row bits of the unit
     bool any_bad = false;
     unsigned long long npos = 0;
-    const uint32_t tbase = tmem_base + (uint32_t(q * 32) << 16);
+    uint32_t lu = 0;
+    for (int u = cid; u < p.units; u += ncl, ++lu) {
+      int nb, mb, ks0, ks1, split;
+      unit_coords<CS>(p, u, crank, nb, mb, ks0, ks1, split);
+      const bool ghost = nb >= p.NB;
+      const int n0 = nb * C::BN, m0 = mb * MT;
+      const uint32_t acc = lu % NACC, use = lu / NACC;
+      const int n = n0 + q * 32 + lane;
+      const bool n_ok = n < p.N;
+      const float bf = (n_ok && p.bias) ? __ldg(p.bias + n) : 0.f;
+      const double bn = double(bf);
+      // stage the unit's row scales (and which rows are "wide") in shared memory
+      named_bar_sync(1, ET);  // previous unit is done with rs_s / wmask
+      {
+        const double rs = et < MT ? __ldcg(p.rscale + m0 + et) : 0.0;
+        if (et < MT) rs_s[et] = rs;
+        const uint32_t wbits = __ballot_sync(0xffffffffu, rs < 0.0);
+        if (lane == 0 && (et >> 5) < 4) wmask[et >> 5] = wbits;
+      }
+      named_bar_sync(1, ET);
+      mbar_wait(&tfull[acc], use & 1);
+      if (et == 0) TG_STAMP(7, 2 + 2 * lu);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + acc * C::ACC_COLS + (uint32_t(q * 32) << 16);
+      bool final_writer = p.splits == 1;
+      float* yrow = p.Y + int64_t(m0) * p.ldy + n;
 #pragma unroll 1
-    for (int mm = 0; mm < MT; mm += 16) {
-      uint32_t r0[16], r1[16], r2[16];
-      tmem_ld16(tbase + mm, r0);
-      tmem_ld16(tbase + MT + mm, r1);
-      tmem_ld16(tbase + 2 * MT + mm, r2);
-      tmem_ld_wait();
+      for (int mm = 16 * half; mm < MT; mm += 32) {
+        uint32_t r0[16], r1[16], r2[16];
+#ifdef TG_EPI_NOLDTM
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int m = m0 + mm + j;
-        if (m < M && n_ok) {
-          const long long tot = (static_cast<long long>(static_cast<int>(r0[j])) << 16) +
-                                (static_cast<long long>(static_cast<int>(r1[j])) << 8) +
-                                static_cast<long long>(static_cast<int>(r2[j]));
-          const double rs = __ldg(rscale + m);  // < 0: wide row, the fix-up kernel owns its count
-          const double v = static_cast<double>(tot) * fabs(rs) + bn;
-          float y = static_cast<float>(v);
-          if (use_alpha && !(y > 0.f)) {
-            y = alpha * y;
-            npos += rs >= 0.0;
+        for (int j = 0; j < 16; ++j) r0[j] = r1[j] = r2[j] = uint32_t(j + mm + et);
+#else
+        tmem_ld16(tbase + mm, r0);
+        tmem_ld16(tbase + MT + mm, r1);
+        tmem_ld16(tbase + 2 * MT + mm, r2);
+        tmem_ld_wait();
+#endif
+        if (et == 0 && lu == 0) TG_STAMP(7, 100 + mm / 16);
+        long long tot[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          tot[j] = (static_cast<long long>(static_cast<int>(r0[j])) << 16) +
+                   (static_cast<long long>(static_cast<int>(r1[j])) << 8) +
+                   static_cast<long long>(static_cast<int>(r2[j]));
+        if (p.splits == 1) {
+          emit16(tot, rs_addr + uint32_t(mm) * 8u, bn, p, m0 + mm, n_ok, yrow + int64_t(mm) * p.ldy, npos, any_bad);
+        } else if (!ghost) {
+          long long* dst = p.part + (int64_t(split) * p.M_pad + m0 + mm) * p.N_pad + n;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) dst[int64_t(j) * p.N_pad] = tot[j];
+        }
+      }
+      // TMEM buffer can be reused by the MMA warp
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (et == 0 && lu == 0) TG_STAMP(7, 120);
+
+      if (p.splits > 1 && !ghost) {
+        // last-arriving unit of this (mb, nb) tile reduces the int64 partials
+        __threadfence();
+        named_bar_sync(1, ET);
+        if (et == 0) {
+          const int old = atomicAdd(p.counters + (mb * p.NB + nb), 1);
+          const int last = old == p.splits - 1;
+          if (last) p.counters[mb * p.NB + nb] = 0;  // reset for the next launch
+          *last_flag = last;
+        }
+        named_bar_sync(1, ET);
+        final_writer = *last_flag != 0;
+        if (final_writer) {
+          __threadfence();
+#pragma unroll 1
+          for (int j0 = 16 * half; j0 < MT; j0 += 32) {
+            // 16 independent rows per batch so the L2 reads of the partials overlap
+            long long tot[16];
+            const long long* src = p.part + int64_t(m0 + j0) * p.N_pad + n;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) tot[j] = __ldcg(src + int64_t(j) * p.N_pad);
+#pragma unroll 1
+            for (int sp = 1; sp < p.splits; ++sp) {
+              const long long* s2 = src + int64_t(sp) * p.M_pad * p.N_pad;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) tot[j] += __ldcg(s2 + int64_t(j) * p.N_pad);
+            }
+            emit16(tot, rs_addr + uint32_t(j0) * 8u, bn, p, m0 + j0, n_ok, yrow + int64_t(j0) * p.ldy, npos,
+                   any_bad);
           }
-          any_bad |= !isfinite(y);
-          Y[int64_t(m) * ldy + n] = y;
+        }
+        named_bar_sync(1, ET);  // last_flag is reused by the next unit
+      }
+      if (et == 0 && lu == 0) TG_STAMP(7, 121);
+      // exact-order recomputation of wide rows in this tile (usually none)
+      if (final_writer && p.fix_var >= 0 && n_ok) {
+#pragma unroll 1
+        for (int w = 0; w < (MT + 31) / 32; ++w) {
+          uint32_t bits = wmask[w];
+          while (bits) {
+            const int j = 32 * w + (__ffs(bits) - 1);
+            bits &= bits - 1;
+            const int m = m0 + j;
+            if (m >= p.M || ((j >> 4) & 1) != half) continue;
+            float y = column_value_row(p.fix_var, p.fix, n, bf, p.X + int64_t(m) * p.ldx, m < p.m_full);
+            if (p.use_alpha && !(y > 0.f)) {
+              y = p.alpha * y;
+              ++npos;
+            }
+            any_bad |= !isfinite(y);
+            p.Y[int64_t(m) * p.ldy + n] = y;
+          }
         }
       }
     }
-    if (flags) {
-      if (__any_sync(0xffffffffu, any_bad) && lane == 0) atomicOr(&flags->nonfinite_output, 1);
+    if (et == 0) TG_STAMP(7, 3 + 2 * (lu - 1));
+    if (p.flags) {
+      if (__any_sync(0xffffffffu, any_bad) && lane == 0) atomicOr(&p.flags->nonfinite_output, 1);
       for (int o = 16; o; o >>= 1) npos += __shfl_xor_sync(0xffffffffu, npos, o);
       if (lane == 0 && npos)
-        atomicAdd(reinterpret_cast<unsigned long long*>(&flags->nonpositive_outputs), npos);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&p.flags->nonpositive_outputs), npos);
     }
-    tc_fence_before();
   }
   __syncwarp();
+  tc_fence_before();
   __syncthreads();
+  if (CS > 1) cluster_sync_all();  // no CTA leaves while peers may still multicast to it
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<C::TMEM_COLS>(tmem_base);
   }
+  if (threadIdx.x == 0) TG_STAMP(7, 500);
 }
 
 // ------------------------------------------------------------------ pack
@@ -427,97 +820,256 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-template <int MT, int STAGES>
-static int launch_mma(const CUtensorMap& map, const uint32_t* tiles, const double* rscale, const float* bias,
-                      float* Y, int64_t ldy, int64_t M, int64_t N, int64_t KC, int64_t M_pad, int64_t N_pad,
-                      int use_alpha, float alpha, tg_device_flags* flags, cudaStream_t st) {
-  using C = MmaCfg<MT, STAGES>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tg_mma_kernel<MT, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(tg_mma_kernel)");
-    attr_set = true;
+static int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
   }
-  dim3 grid(unsigned(N_pad / C::BN), unsigned(M_pad / MT));
-  tg_mma_kernel<MT, STAGES><<<grid, 192, C::SMEM, st>>>(map, tiles, rscale, bias, Y, ldy, int(M), int(N),
-                                                         int(KC), int(M_pad), int(N_pad), use_alpha, alpha,
-                                                         flags);
-  return check_launch("tg_mma_kernel");
+  return n;
 }
 
 int mma_pick_mt(int64_t M) {
   if (M <= 16) return 16;
   if (M <= 32) return 32;
-  return 64;
+  if (M <= 48) return 48;
+  return 64;  // N = 192: two TMEM accumulators + a 4-slot A ring fit the 512 columns
+}
+
+// K splits per (column group, row block) tile: minimise rounds x (stages + overhead)
+// over a persistent grid of `slots` clusters.  Integer accumulation makes any split exact.
+static int pick_splits(int64_t base_units, int64_t KC, int slots) {
+  int best = 1;
+  int64_t best_cost = INT64_MAX;
+  const int64_t smax = std::min<int64_t>(KC, 16);
+  for (int64_t s = 1; s <= smax; ++s) {
+    const int64_t rounds = ceil_div(base_units * s, slots);
+    const int64_t cost = rounds * (ceil_div(KC, s) + (s > 1 ? 2 : 0));
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = int(s);
+    }
+  }
+  return best;
+}
+
+// Cluster size: the X-limb tile of a row block is multicast to CS CTAs that
+// work on CS adjacent column blocks, cutting the L2->SM traffic (the bound of
+// the 1-CTA kernel) by CS.  Slices must be whole 8-row swizzle atoms.
+static int pick_cluster(int64_t mt, int64_t NB) {
+  int cs = mt >= 64 ? 4 : mt >= 32 ? (mt == 48 ? 2 : 4) : 1;
+  if (const char* env = getenv("TG_MMA_CLUSTER")) {
+    const int v = atoi(env);
+    if (v == 1 || v == 2 || v == 4) cs = v;
+  }
+  while (cs > 1 && (mt / cs < 8 || (mt / cs) % 8 != 0)) cs /= 2;
+  while (cs > 1 && NB < cs) cs /= 2;
+  return cs;
+}
+
+template <int MT, int CS>
+static int max_clusters() {
+  static int n = 0;
+  if (n == 0) {
+    using C = MmaCfg<MT>;
+    cudaFuncSetAttribute(tg_mma_kernel<MT, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (CS > 1) cudaFuncSetAttribute(tg_mma_kernel<MT, CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(CS * 256));
+    cfg.blockDim = dim3(C::THREADS);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int c = 0;
+    if (cudaOccupancyMaxActiveClusters(&c, tg_mma_kernel<MT, CS>, &cfg) != cudaSuccess || c <= 0) {
+      cudaGetLastError();
+      c = num_sms() / CS;
+    }
+    n = c;
+  }
+  return n;
+}
+
+static int max_clusters_for(int64_t mt, int cs) {
+  switch (mt * 10 + cs) {
+    case 161: return max_clusters<16, 1>();
+    case 162: return max_clusters<16, 2>();
+    case 321: return max_clusters<32, 1>();
+    case 322: return max_clusters<32, 2>();
+    case 324: return max_clusters<32, 4>();
+    case 481: return max_clusters<48, 1>();
+    case 482: return max_clusters<48, 2>();
+    case 641: return max_clusters<64, 1>();
+    case 642: return max_clusters<64, 2>();
+    default: return max_clusters<64, 4>();
+  }
 }
 
 struct SplitLayout {
-  int64_t mt, M_pad, K_pad;
-  size_t off_rscale, off_wide, total;
+  int64_t mt, M_pad, K_pad, N_pad, KC, MB, NB, NBG;
+  int splits, cs, clusters;
+  size_t off_rscale, off_counters, off_part, total_prepare, total;
 };
 
-static SplitLayout split_layout(int64_t M, int64_t K) {
+static SplitLayout split_layout(int64_t M, int64_t K, int64_t N) {
   SplitLayout L;
   L.mt = mma_pick_mt(M);
   L.M_pad = round_up(M, L.mt);
   L.K_pad = round_up(K, 128);
+  L.KC = L.K_pad / 128;
+  L.MB = L.M_pad / L.mt;
+  L.N_pad = N > 0 ? round_up(N, 128) : 0;
+  L.NB = L.N_pad / 128;
+  L.cs = N > 0 ? pick_cluster(L.mt, L.NB) : 1;
+  L.NBG = ceil_div(L.NB, L.cs);
+  L.clusters = N > 0 ? max_clusters_for(L.mt, L.cs) : 1;
+  L.splits = N > 0 ? pick_splits(L.MB * L.NBG, ceil_div(L.KC, 2), L.clusters) : 1;
   L.off_rscale = size_t(round_up(3 * L.M_pad * L.K_pad, 256));
-  L.off_wide = L.off_rscale + size_t(round_up(L.M_pad * int64_t(sizeof(double)), 256));
-  L.total = L.off_wide + size_t(round_up((L.M_pad + 1) * 4, 256));
+  L.total_prepare = L.off_rscale + size_t(round_up(L.M_pad * int64_t(sizeof(double)), 256));
+  L.off_counters = L.total_prepare;
+  L.off_part = L.off_counters + size_t(round_up(L.MB * L.NB * 4, 256));
+  L.total = L.splits > 1 ? L.off_part + size_t(L.splits) * size_t(L.M_pad) * size_t(L.N_pad) * 8 : L.total_prepare;
   return L;
 }
 
-size_t xsplit_bytes(int64_t M, int64_t K) { return split_layout(M, K).total; }
-
-const int32_t* wide_rows(void* ws, int64_t M, int64_t K) {
-  return reinterpret_cast<const int32_t*>(static_cast<uint8_t*>(ws) + split_layout(M, K).off_wide);
-}
+size_t xsplit_bytes(int64_t M, int64_t K) { return split_layout(M, K, 0).total_prepare; }
+size_t mma_ws_bytes(int64_t M, int64_t K, int64_t N) { return split_layout(M, K, N).total; }
 
 int run_xsplit(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size_t ws_bytes, tg_device_flags* flags,
                cudaStream_t st) {
-  const SplitLayout L = split_layout(M, K);
-  if (ws_bytes < L.total) return set_error(TG_ERR_PARAM, "workspace too small for X split");
+  const SplitLayout L = split_layout(M, K, 0);
+  if (ws_bytes < L.total_prepare) return set_error(TG_ERR_PARAM, "workspace too small for X split");
   uint8_t* base = static_cast<uint8_t*>(ws);
   int8_t* limbs = reinterpret_cast<int8_t*>(base);
   double* rscale = reinterpret_cast<double*>(base + L.off_rscale);
-  int32_t* wide = reinterpret_cast<int32_t*>(base + L.off_wide);
-  cudaError_t e = cudaMemsetAsync(wide, 0, sizeof(int32_t), st);
-  if (e != cudaSuccess) return set_cuda_error(e, "cudaMemsetAsync(wide rows)");
-  tg_xsplit_kernel<<<unsigned(L.M_pad), 256, 0, st>>>(X, M, K, ldx, limbs, rscale, wide, L.M_pad, L.K_pad, flags);
+  cudaError_t e = cudaSuccess;
+  if (K <= XS_SMEM_MAX_K) {
+    const size_t smem = size_t(round_up(K, 4)) * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      e = cudaFuncSetAttribute(tg_xsplit_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(XS_SMEM_MAX_K * sizeof(float)));
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(tg_xsplit_kernel<true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(XS_SMEM_MAX_K * sizeof(float)));
+      if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(tg_xsplit_kernel)");
+      attr = true;
+    }
+    // few rows: more threads per row so the whole GPU has loads in flight
+    if (L.M_pad <= 4 * num_sms())
+      tg_xsplit_kernel<true, 1024><<<unsigned(L.M_pad), 1024, smem, st>>>(X, M, K, ldx, limbs, rscale,
+                                                                          L.M_pad, L.K_pad, flags);
+    else
+      tg_xsplit_kernel<true, 256><<<unsigned(L.M_pad), 256, smem, st>>>(X, M, K, ldx, limbs, rscale, L.M_pad,
+                                                                        L.K_pad, flags);
+  } else {
+    tg_xsplit_kernel<false, 256><<<unsigned(L.M_pad), 256, 0, st>>>(X, M, K, ldx, limbs, rscale, L.M_pad,
+                                                                     L.K_pad, flags);
+  }
   return check_launch("tg_xsplit_kernel");
 }
 
-int run_mma(int64_t M, int64_t K, const uint32_t* tiles, int64_t N, const float* bias, float* Y, int64_t ldy,
-            int use_alpha, float alpha, void* ws, tg_device_flags* flags, cudaStream_t st) {
-  const SplitLayout L = split_layout(M, K);
-  const int64_t mt = L.mt, M_pad = L.M_pad, K_pad = L.K_pad;
-  const int64_t N_pad = round_up(N, 128);
-  const int64_t KC = K_pad / 128;
-  int8_t* limbs = static_cast<int8_t*>(ws);
-  double* rscale = reinterpret_cast<double*>(static_cast<uint8_t*>(ws) + L.off_rscale);
+template <int MT, int CS>
+static int launch_mma(const CUtensorMap& map, const MmaParams& p, int grid, cudaStream_t st) {
+  using C = MmaCfg<MT>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(tg_mma_kernel<MT, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(tg_mma_kernel)");
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap our prologue with the X split
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = CS;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = CS > 1 ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tg_mma_kernel<MT, CS>, map, p);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaLaunchKernelEx(tg_mma_kernel)");
+  return check_launch("tg_mma_kernel");
+}
+
+int run_mma(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N, const float* bias,
+            float* Y, int64_t ldy, int use_alpha, float alpha, const MmaFixup* fix, void* ws, size_t ws_bytes,
+            tg_device_flags* flags, cudaStream_t st) {
+  const SplitLayout L = split_layout(M, K, N);
+  if (ws_bytes < L.total) return set_error(TG_ERR_PARAM, "workspace too small for the tensor-core path");
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  int8_t* limbs = reinterpret_cast<int8_t*>(base);
 
   auto enc = get_encode();
   if (!enc) return set_error(TG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap map;
-  cuuint64_t gdim[2] = {cuuint64_t(K_pad), cuuint64_t(3 * M_pad)};
-  cuuint64_t gstride[1] = {cuuint64_t(K_pad)};
-  cuuint32_t box[2] = {128u, cuuint32_t(mt)};
+  cuuint64_t gdim[2] = {cuuint64_t(L.K_pad), cuuint64_t(3 * L.M_pad)};
+  cuuint64_t gstride[1] = {cuuint64_t(L.K_pad)};
+  cuuint32_t box[2] = {128u, cuuint32_t(L.mt / L.cs)};  // each cluster CTA loads (and multicasts) one slice
   cuuint32_t estride[2] = {1u, 1u};
   CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, limbs, gdim, gstride, box, estride,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(TG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-  switch (mt) {
-    case 16:
-      return launch_mma<16, 6>(map, tiles, rscale, bias, Y, ldy, M, N, KC, M_pad, N_pad, use_alpha, alpha,
-                               flags, st);
-    case 32:
-      return launch_mma<32, 5>(map, tiles, rscale, bias, Y, ldy, M, N, KC, M_pad, N_pad, use_alpha, alpha,
-                               flags, st);
-    default:
-      return launch_mma<64, 4>(map, tiles, rscale, bias, Y, ldy, M, N, KC, M_pad, N_pad, use_alpha, alpha,
-                               flags, st);
+
+  MmaParams p{};
+  p.tiles = tiles;
+  p.rscale = reinterpret_cast<const double*>(base + L.off_rscale);
+  p.bias = bias;
+  p.Y = Y;
+  p.ldy = ldy;
+  p.M = int(M);
+  p.N = int(N);
+  p.KC = int(L.KC);
+  p.KS = int(ceil_div(L.KC, 2));
+  p.M_pad = int(L.M_pad);
+  p.N_pad = int(L.N_pad);
+  p.MB = int(L.MB);
+  p.NB = int(L.NB);
+  p.NBG = int(L.NBG);
+  p.splits = L.splits;
+  p.units = int(L.MB * L.NBG * L.splits);
+  p.use_alpha = use_alpha;
+  p.alpha = alpha;
+  p.flags = flags;
+  p.fix_var = -1;
+  if (fix) {
+    p.fix_var = fix->var;
+    p.m_full = fix->m_full;
+    p.fix = fix->args;
+    p.X = X;
+    p.ldx = ldx;
+  }
+  if (L.splits > 1) {
+    p.counters = reinterpret_cast<int32_t*>(base + L.off_counters);
+    p.part = reinterpret_cast<long long*>(base + L.off_part);
+    cudaError_t e = cudaMemsetAsync(p.counters, 0, size_t(L.MB * L.NB) * 4, st);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaMemsetAsync(split counters)");
+  }
+  const int grid = int(std::min<int64_t>(p.units, L.clusters)) * L.cs;
+  switch (L.mt * 10 + L.cs) {
+    case 161: return launch_mma<16, 1>(map, p, grid, st);
+    case 162: return launch_mma<16, 2>(map, p, grid, st);
+    case 321: return launch_mma<32, 1>(map, p, grid, st);
+    case 322: return launch_mma<32, 2>(map, p, grid, st);
+    case 324: return launch_mma<32, 4>(map, p, grid, st);
+    case 481: return launch_mma<48, 1>(map, p, grid, st);
+    case 482: return launch_mma<48, 2>(map, p, grid, st);
+    case 641: return launch_mma<64, 1>(map, p, grid, st);
+    case 642: return launch_mma<64, 2>(map, p, grid, st);
+    default: return launch_mma<64, 4>(map, p, grid, st);
   }
 }
 
@@ -578,3 +1130,9 @@ int run_unpack_dense(const uint32_t* tiles, int64_t K, int64_t N, int8_t* W, cud
 }
 
 }  // namespace tg
+
+#ifdef TG_TRACE
+extern "C" int tg_debug_trace(unsigned long long* host_out) {
+  return cudaMemcpyFromSymbol(host_out, tg::g_tg_trace, sizeof(tg::g_tg_trace)) == cudaSuccess ? 0 : 3;
+}
+#endif

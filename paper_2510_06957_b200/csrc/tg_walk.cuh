@@ -1,0 +1,186 @@
+// tg_walk.cuh — exact-order evaluation of one output column over the
+// reference's own index streams.  Shared by the CUDA-core gather kernels
+// (tg_gather.cu) and the wide-row fix-up inside the tensor-core epilogue
+// (tg_mma.cu).  Every function reproduces the fp32 operation order of the
+// reference kernel it names, so results are bit-identical to it:
+//
+//   VAR_BASE      kernels/scalar.py:109-132  acc=0; acc+=x (pos); acc-=x (neg); out=b+acc
+//   VAR_UNROLLED  kernels/scalar.py:156-257  uf accumulator banks; bank u takes stream
+//                 positions start+u, start+u+uf, ...; the tail of each sign goes to
+//                 bank 0; tot = ((0 + bank0) + bank1) + ...; out = b + tot
+//   VAR_BLOCKED   kernels/scalar.py:286-367  out=b; per block: rows m < floor(M/mr)*mr use the
+//                 banked sum (out += tot), the leftover rows acc=0; +pos; -neg; out+=acc
+//   VAR_IB        kernels/scalar.py:397-485  out=b; per block: acc=0; runs of g (+,-); +rem; -rem; out+=acc
+//   VAR_OPTIMAL   kernels/simd.py:282-420    out=b; per block: acc over the interleaved segment
+//                 (sign = parity of t//g); out+=acc; out+=x (pos rem); out-=x (neg rem)
+#pragma once
+#include <cstdint>
+
+namespace tg {
+
+enum { VAR_BASE = 0, VAR_BLOCKED = 1, VAR_IB = 2, VAR_OPTIMAL = 3, VAR_UNROLLED = 4 };
+
+__device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ void add_(float4& a, const float4 b) {
+  a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+}
+__device__ __forceinline__ void sub_(float4& a, const float4 b) {
+  a.x -= b.x; a.y -= b.y; a.z -= b.z; a.w -= b.w;
+}
+__device__ __forceinline__ void add_(float& a, const float b) { a += b; }
+__device__ __forceinline__ void sub_(float& a, const float b) { a -= b; }
+template <typename V> __device__ __forceinline__ V zero_();
+template <> __device__ __forceinline__ float zero_<float>() { return 0.f; }
+template <> __device__ __forceinline__ float4 zero_<float4>() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+template <typename V> __device__ __forceinline__ V splat_(float b);
+template <> __device__ __forceinline__ float splat_<float>(float b) { return b; }
+template <> __device__ __forceinline__ float4 splat_<float4>(float b) { return make_float4(b, b, b, b); }
+// b + acc (scalar.py:127 `bias[n] + acc`), component-wise
+__device__ __forceinline__ float badd_(float b, float a) { return b + a; }
+__device__ __forceinline__ float4 badd_(float b, float4 a) { return make_float4(b + a.x, b + a.y, b + a.z, b + a.w); }
+
+// Operand sources: the value X[., k] for a stream index k.
+struct SrcXt {  // 4 consecutive rows from the transposed copy Xt[K+1][M_pad]
+  using V = float4;
+  const float* xt;
+  int64_t ld;
+  __device__ __forceinline__ float4 operator()(int32_t k) const { return ld4(xt + int64_t(k) * ld); }
+};
+struct SrcRow {  // one row of X in place (ldx = K or K+1)
+  using V = float;
+  const float* x;
+  __device__ __forceinline__ float operator()(int32_t k) const { return __ldg(x + k); }
+};
+
+// Walk [a, b) of an index stream adding (NEG=false) or subtracting into acc,
+// strictly in stream order.
+template <bool NEG, typename S>
+__device__ __forceinline__ void walk(typename S::V& acc, const int32_t* __restrict__ idx, int32_t a, int32_t b,
+                                     const S& src) {
+  int32_t i = a;
+  for (; i + 4 <= b; i += 4) {
+    const int32_t k0 = __ldg(idx + i), k1 = __ldg(idx + i + 1), k2 = __ldg(idx + i + 2), k3 = __ldg(idx + i + 3);
+    const typename S::V v0 = src(k0), v1 = src(k1), v2 = src(k2), v3 = src(k3);
+    if (NEG) { sub_(acc, v0); sub_(acc, v1); sub_(acc, v2); sub_(acc, v3); }
+    else { add_(acc, v0); add_(acc, v1); add_(acc, v2); add_(acc, v3); }
+  }
+  for (; i < b; ++i) {
+    const typename S::V v = src(__ldg(idx + i));
+    if (NEG) sub_(acc, v); else add_(acc, v);
+  }
+}
+
+// Interleaved segment [s0, s1): alternating runs of g, positives first.
+template <typename S>
+__device__ __forceinline__ void walk_interleaved(typename S::V& acc, const int32_t* __restrict__ ai, int32_t s0,
+                                                 int32_t s1, int g, const S& src) {
+  for (int32_t i = s0; i < s1; i += 2 * g) {
+    walk<false>(acc, ai, i, min(i + g, s1), src);
+    walk<true>(acc, ai, min(i + g, s1), min(i + 2 * g, s1), src);
+  }
+}
+
+// Banked sum of one (pos, neg) cell, kernels/scalar.py:167-206: every bank is an
+// independent sequential accumulation, so the banks are evaluated one after the
+// other and folded into tot in bank order -- two live accumulators for any uf.
+template <typename S>
+__device__ __forceinline__ typename S::V banked_sum(const int32_t* __restrict__ rp, int32_t ap, int32_t bp,
+                                                    const int32_t* __restrict__ rn, int32_t an, int32_t bn, int uf,
+                                                    const S& src) {
+  using V = typename S::V;
+  V tot = zero_<V>();
+  const int32_t fp = ap + (bp - ap) / uf * uf, fn = an + (bn - an) / uf * uf;
+  for (int u = 0; u < uf; ++u) {
+    V bank = zero_<V>();
+    for (int32_t i = ap + u; i < fp; i += uf) add_(bank, src(__ldg(rp + i)));
+    if (u == 0) walk<false>(bank, rp, fp, bp, src);
+    for (int32_t i = an + u; i < fn; i += uf) sub_(bank, src(__ldg(rn + i)));
+    if (u == 0) walk<true>(bank, rn, fn, bn, src);
+    add_(tot, bank);
+  }
+  return tot;
+}
+
+struct GatherArgs {
+  const int32_t* p0;  // col_start_pos (TCSC / blocked) or col_segment_ptr (interleaved)
+  const int32_t* i0;  // row_index_pos or all_indices
+  const int32_t* p1;  // col_start_neg
+  const int32_t* i1;  // row_index_neg
+  int64_t N, nblocks, m_full;
+  int g, uf;
+};
+
+// Y[m, n] before the activation, in the reference's operation order for VAR.
+// `banked_rows` (blocked only): bit r set if component r belongs to a row < m_full.
+template <int VAR, typename S>
+__device__ __forceinline__ typename S::V column_value(const GatherArgs& a, int64_t n, float b, const S& src,
+                                                      unsigned banked_rows) {
+  using V = typename S::V;
+  if (VAR == VAR_BASE) {
+    V acc = zero_<V>();
+    walk<false>(acc, a.i0, __ldg(a.p0 + n), __ldg(a.p0 + n + 1), src);
+    walk<true>(acc, a.i1, __ldg(a.p1 + n), __ldg(a.p1 + n + 1), src);
+    return badd_(b, acc);
+  } else if (VAR == VAR_UNROLLED) {
+    const V tot = banked_sum(a.i0, __ldg(a.p0 + n), __ldg(a.p0 + n + 1), a.i1, __ldg(a.p1 + n), __ldg(a.p1 + n + 1),
+                             a.uf, src);
+    return badd_(b, tot);
+  } else if (VAR == VAR_BLOCKED) {
+    V out = splat_<V>(b);
+    for (int64_t blk = 0; blk < a.nblocks; ++blk) {
+      const int32_t* cp = a.p0 + blk * (a.N + 1);
+      const int32_t* cn = a.p1 + blk * (a.N + 1);
+      const int32_t ap = __ldg(cp + n), bp = __ldg(cp + n + 1), an = __ldg(cn + n), bn = __ldg(cn + n + 1);
+      V tot = zero_<V>(), acc = zero_<V>();
+      if (banked_rows) tot = banked_sum(a.i0, ap, bp, a.i1, an, bn, a.uf, src);
+      if (banked_rows != (sizeof(V) == 4 ? 1u : 15u)) {
+        walk<false>(acc, a.i0, ap, bp, src);
+        walk<true>(acc, a.i1, an, bn, src);
+      }
+      if constexpr (sizeof(V) == 4) {
+        out += (banked_rows & 1u) ? tot : acc;
+      } else {
+        out.x += (banked_rows & 1u) ? tot.x : acc.x;
+        out.y += (banked_rows & 2u) ? tot.y : acc.y;
+        out.z += (banked_rows & 4u) ? tot.z : acc.z;
+        out.w += (banked_rows & 8u) ? tot.w : acc.w;
+      }
+    }
+    return out;
+  } else {
+    V out = splat_<V>(b);
+    for (int64_t blk = 0; blk < a.nblocks; ++blk) {
+      const int64_t cell = blk * a.N + n;
+      const int32_t s0 = __ldg(a.p0 + 3 * cell), s1 = __ldg(a.p0 + 3 * cell + 1);
+      const int32_t s2 = __ldg(a.p0 + 3 * cell + 2), s3 = __ldg(a.p0 + 3 * cell + 3);
+      V acc = zero_<V>();
+      walk_interleaved(acc, a.i0, s0, s1, a.g, src);
+      if (VAR == VAR_IB) {
+        walk<false>(acc, a.i0, s1, s2, src);
+        walk<true>(acc, a.i0, s2, s3, src);
+        add_(out, acc);
+      } else {
+        add_(out, acc);
+        walk<false>(out, a.i0, s1, s2, src);
+        walk<true>(out, a.i0, s2, s3, src);
+      }
+    }
+    return out;
+  }
+}
+
+// Runtime dispatch of the one-row (SrcRow) evaluation, for the fix-up paths.
+__device__ __forceinline__ float column_value_row(int var, const GatherArgs& a, int64_t n, float b, const float* xrow,
+                                                  bool banked) {
+  const SrcRow src{xrow};
+  const unsigned br = banked ? 1u : 0u;
+  switch (var) {
+    case VAR_BASE: return column_value<VAR_BASE>(a, n, b, src, br);
+    case VAR_UNROLLED: return column_value<VAR_UNROLLED>(a, n, b, src, br);
+    case VAR_BLOCKED: return column_value<VAR_BLOCKED>(a, n, b, src, br);
+    case VAR_IB: return column_value<VAR_IB>(a, n, b, src, br);
+    default: return column_value<VAR_OPTIMAL>(a, n, b, src, br);
+  }
+}
+
+}  // namespace tg
