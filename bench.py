@@ -288,9 +288,14 @@ def run_ours(args) -> None:
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
     stream = torch.cuda.current_stream()
 
+    graph = None if args.no_graph else runner.capture()
+
     def step():
-        runner.launch(stage="prepare")
-        runner.launch(stage="run")
+        if graph is not None:
+            graph.replay()
+        else:
+            runner.launch(stage="prepare")
+            runner.launch(stage="run")
         if world > 1:
             part.assemble(runner.y, y_full)
 
@@ -454,7 +459,8 @@ def run_ours(args) -> None:
         "config": {"workload": cfg, "M": M, "K": K, "N": N, "p_nonzero": wl.p_pos + wl.p_neg, "nnz": nnz_total,
                    "alpha": wl.alpha, "variant": wl.variant, "method": method,
                    "parallelism": f"N-sharded x{world}" + (" + NCCL all-gather" if world > 1 else ""),
-                   "l2": "flushed (256 MB write) before every timed step, outside the events"},
+                   "l2": "flushed (256 MB write) before every timed step, outside the events",
+                   "launch": "CUDA graph replay per step" if graph is not None else "direct launches"},
         "breakdown_ms": {"prepare": round(t_prep, 5), "run": round(t_run, 5), "assemble": round(t_comm, 5),
                          "note": "separate pass with events between stages (no PDL overlap); headline is whole steps"},
         "roofline": roof,
@@ -482,6 +488,7 @@ def main() -> None:
     ap.add_argument("--method", default="auto", choices=("auto", "mma", "gather"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the public-API end-to-end leg (profiling runs)")
+    ap.add_argument("--no-graph", action="store_true", help="issue the step's kernels one by one instead of a CUDA graph")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -42,6 +42,36 @@
 
 namespace tg {
 
+// ------------------------------------------------------------------ trace (debug builds only)
+#ifdef TG_TRACE
+// [cta slot][event][iteration]: clock64 stamps of CTA 0 and CTA 1, first 512 pipeline iterations
+__device__ unsigned long long g_tg_trace[2][8][512];
+#define TG_STAMP(ev, it)                                                           \
+  do {                                                                             \
+    if (blockIdx.x < 2 && (it) < 512) g_tg_trace[blockIdx.x][ev][it] = clock64(); \
+  } while (0)
+// global-time (ns) milestones of the whole step: [ev][0] = min over CTAs, [ev][1] = max
+__device__ unsigned long long g_tg_gt[16][2];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TG_GT(ev)                                           \
+  do {                                                      \
+    const unsigned long long _t = gtime();                  \
+    atomicMin(&g_tg_gt[ev][0], _t);                         \
+    atomicMax(&g_tg_gt[ev][1], _t);                         \
+  } while (0)
+#else
+#define TG_STAMP(ev, it) \
+  do {                   \
+  } while (0)
+#define TG_GT(ev) \
+  do {            \
+  } while (0)
+#endif
+
 // ------------------------------------------------------------------ X split
 // One CTA per (padded) row.  limbs: [3][M_pad][K_pad] int8, rscale: [M_pad] f64.
 //
@@ -52,6 +82,10 @@ namespace tg {
 // gets its rscale stored negated: the MMA epilogue then recomputes the row in
 // the exact reference order (and takes its PReLU count there).
 constexpr float kWideRatio = 16.f;
+// The epilogue applies 2^-s and 2^(24-s) as normal floats: |s| <= 100 keeps both
+// (and every partial product) far inside the fp32 range.  Rows outside take the
+// exact-order path.
+constexpr int kMaxScaleExp = 100;
 constexpr int64_t XS_SMEM_MAX_K = 16384;  // rows up to 64 KB are staged in shared memory
 
 template <int XS_THREADS>
@@ -186,9 +220,128 @@ __global__ void __launch_bounds__(XS_THREADS) tg_xsplit_kernel(const float* __re
   s2 = block_sum<XS_THREADS>(s2, red);
   nzf = block_sum<XS_THREADS>(nzf, red);
   if (threadIdx.x == 0) {
-    const bool is_wide = live && nzf > kWideRatio * kWideRatio * s2;  // amax / rms(nonzeros) > kWideRatio
+    // amax / rms(nonzeros) > kWideRatio, or a scale outside the epilogue's fp32 range
+    const bool is_wide = live && (nzf > kWideRatio * kWideRatio * s2 || s > kMaxScaleExp || s < -kMaxScaleExp);
     const double sc = live ? ldexp(1.0, -s) : 0.0;
     rscale[m] = is_wide ? -sc : sc;
+  }
+}
+
+// Register-resident variant: thread t owns EPT consecutive k of the row, so the
+// row is read once, reduced once (amax, sum x^2 in fp64, nonzero count) and
+// converted from registers.  Digits: with |v| < 2^22, u = v + 0x808080 lies in
+// [0, 2^24) and byte i of u, minus 128, is the i-th balanced base-256 digit of v
+// (the same digits as limb_digits); as int8 that is byte ^ 0x80.
+template <int THREADS, int EPT>
+__global__ void __launch_bounds__(THREADS) tg_xsplit_reg_kernel(const float* __restrict__ X, int64_t M, int64_t K,
+                                                                int64_t ldx, int8_t* __restrict__ limbs,
+                                                                double* __restrict__ rscale, int64_t M_pad,
+                                                                int64_t K_pad, tg_device_flags* __restrict__ flags) {
+  static_assert(EPT % 4 == 0, "EPT");
+  constexpr int NW = THREADS / 32;
+  __shared__ float red_f[NW];
+  __shared__ double red_d[NW];
+  __shared__ int red_i[NW];
+  grid_dep_launch();  // the MMA kernel may start its prologue (it waits before reading our output)
+  if (threadIdx.x == 0) TG_GT(0);
+  const int64_t m = blockIdx.x;
+  const float* grow = X + m * ldx;
+  const int64_t k0 = int64_t(threadIdx.x) * EPT;
+  float x[EPT];
+  const bool in = m < M;
+  if (in && k0 + EPT <= K && ((reinterpret_cast<uintptr_t>(grow + k0) & 15) == 0)) {
+#pragma unroll
+    for (int j = 0; j < EPT; j += 4) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(grow + k0 + j));
+      x[j] = v.x; x[j + 1] = v.y; x[j + 2] = v.z; x[j + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) x[j] = (in && k0 + j < K) ? __ldg(grow + k0 + j) : 0.f;
+  }
+  float amax = 0.f;
+  double s2 = 0.0;
+  int nz = 0;
+#pragma unroll
+  for (int j = 0; j < EPT; ++j) {
+    amax = fmaxf(amax, fabsf(x[j]));
+    s2 = fma(double(x[j]), double(x[j]), s2);
+    nz += x[j] != 0.f;
+  }
+  for (int o = 16; o; o >>= 1) {
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    nz += __shfl_xor_sync(0xffffffffu, nz, o);
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red_f[w] = amax;
+    red_d[w] = s2;
+    red_i[w] = nz;
+  }
+  __syncthreads();
+  amax = red_f[0];
+  s2 = red_d[0];
+  nz = red_i[0];
+#pragma unroll
+  for (int i = 1; i < NW; ++i) {
+    amax = fmaxf(amax, red_f[i]);
+    s2 += red_d[i];
+    nz += red_i[i];
+  }
+  const bool finite = amax <= 3.402823466e38f;  // false for inf / nan
+  const bool live = in && amax > 0.f && finite;
+  int s = 0;
+  if (live) {
+    int e;
+    frexpf(amax, &e);  // amax < 2^e
+    s = 22 - e;        // |x * 2^s| < 2^22
+  } else if (in && !finite && threadIdx.x == 0 && flags) {
+    atomicOr(&flags->bad_input, 4);
+  }
+  if (threadIdx.x == 0) {
+    // amax / rms(nonzeros) > kWideRatio  <=>  nz * amax^2 > kWideRatio^2 * sum x^2
+    const bool is_wide = live && (double(nz) * double(amax) * double(amax) > double(kWideRatio * kWideRatio) * s2 ||
+                                  s > kMaxScaleExp || s < -kMaxScaleExp);
+    const double sc = live ? ldexp(1.0, -s) : 0.0;
+    rscale[m] = is_wide ? -sc : sc;
+    TG_GT(1);
+  }
+  if (k0 >= K_pad) return;
+  // x * 2^s as two exact power-of-two multiplies (2^s alone may exceed the float range)
+  const int s_a = s > 126 ? 126 : (s < -126 ? -126 : s);
+  const float sc_a = __int_as_float((127 + s_a) << 23), sc_b = __int_as_float((127 + s - s_a) << 23);
+  uint32_t w0[EPT / 4], w1[EPT / 4], w2[EPT / 4];
+#pragma unroll
+  for (int j = 0; j < EPT; j += 4) {
+    uint32_t u[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) u[i] = uint32_t((live ? __float2int_rn((x[j + i] * sc_a) * sc_b) : 0) + 0x808080);
+    const uint32_t lo01 = __byte_perm(u[0], u[1], 0x5140);  // b0(u0) b0(u1) b1(u0) b1(u1)
+    const uint32_t lo23 = __byte_perm(u[2], u[3], 0x5140);
+    const uint32_t hi01 = __byte_perm(u[0], u[1], 0x7362);  // b2(u0) b2(u1) b3 b3
+    const uint32_t hi23 = __byte_perm(u[2], u[3], 0x7362);
+    w2[j / 4] = __byte_perm(lo01, lo23, 0x5410) ^ 0x80808080u;  // byte 0 of each u: low digit
+    w1[j / 4] = __byte_perm(lo01, lo23, 0x7632) ^ 0x80808080u;  // byte 1: middle digit
+    w0[j / 4] = __byte_perm(hi01, hi23, 0x5410) ^ 0x80808080u;  // byte 2: high digit
+  }
+  int8_t* l0 = limbs + m * K_pad + k0;
+  int8_t* l1 = limbs + (M_pad + m) * K_pad + k0;
+  int8_t* l2 = limbs + (2 * M_pad + m) * K_pad + k0;
+  if constexpr (EPT % 16 == 0) {
+#pragma unroll
+    for (int j = 0; j < EPT / 4; j += 4) {
+      reinterpret_cast<uint4*>(l0)[j / 4] = make_uint4(w0[j], w0[j + 1], w0[j + 2], w0[j + 3]);
+      reinterpret_cast<uint4*>(l1)[j / 4] = make_uint4(w1[j], w1[j + 1], w1[j + 2], w1[j + 3]);
+      reinterpret_cast<uint4*>(l2)[j / 4] = make_uint4(w2[j], w2[j + 1], w2[j + 2], w2[j + 3]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < EPT / 4; ++j) {
+      reinterpret_cast<uint32_t*>(l0)[j] = w0[j];
+      reinterpret_cast<uint32_t*>(l1)[j] = w1[j];
+      reinterpret_cast<uint32_t*>(l2)[j] = w2[j];
+    }
   }
 }
 
@@ -209,20 +362,6 @@ __device__ __forceinline__ uint4 decode_word(uint32_t w) {
   o.w = (x & 0x01010101u) + (x & 0x02020202u) * 0x7Fu;
   return o;
 }
-
-// ------------------------------------------------------------------ trace (debug builds only)
-#ifdef TG_TRACE
-// [cta slot][event][iteration]: clock64 stamps of CTA 0 and CTA 1, first 512 pipeline iterations
-__device__ unsigned long long g_tg_trace[2][8][512];
-#define TG_STAMP(ev, it)                                                           \
-  do {                                                                             \
-    if (blockIdx.x < 2 && (it) < 512) g_tg_trace[blockIdx.x][ev][it] = clock64(); \
-  } while (0)
-#else
-#define TG_STAMP(ev, it) \
-  do {                   \
-  } while (0)
-#endif
 
 // ------------------------------------------------------------------ MMA
 struct MmaParams {
@@ -299,58 +438,66 @@ __device__ __forceinline__ void unit_coords(const MmaParams& p, int u, int crank
   ks1 = int((int64_t(split + 1) * p.KS) / p.splits);
 }
 
-__device__ __forceinline__ float finish(long long tot, double rs, double bn, int use_alpha, float alpha,
-                                        bool count_it, unsigned long long& npos, bool& bad) {
-  const double v = static_cast<double>(tot) * fabs(rs) + bn;
-  float y = static_cast<float>(v);
-  if (use_alpha && !(y > 0.f)) {
-    y = alpha * y;
-    npos += count_it;
-  }
-  bad |= !isfinite(y);
-  return y;
-}
-
-// Finish 16 consecutive rows of one output column: y = fp32(tot * |rs| + b)
-// (tot * |rs| is exact: rs is a power of two), PReLU, store.  Straight-line
-// so the 16 conversions pipeline; rows >= M are not stored.
-__device__ __forceinline__ void emit16(const long long (&tot)[16], uint32_t rs_addr, double bn, const MmaParams& p,
-                                       int m_first, bool n_ok, float* yrow, unsigned long long& npos, bool& bad) {
-  double rs[16];
+// Finish 16 consecutive rows of one output column: y = fp32(tot * 2^-s + b),
+// PReLU, store.  No FP64 and no 64-bit conversions (each costs ~13 issue cycles
+// per warp on B200, scratch/cvt_bench.cu): tot = H 2^24 + L with 0 <= L < 2^24,
+// so float(H), float(L) are exact and y = fma(H, 2^(24-s), fma(L, 2^-s, b)).
+// The per-row scales {2^-s, 2^(24-s)} are staged as float2 in shared memory;
+// rows whose scale leaves the float range are "wide" and recomputed exactly.
+// Straight-line so the 16 rows pipeline; rows >= M are not stored.
+__device__ __forceinline__ void emit16(const long long (&tot)[16], uint32_t sc_addr, float bf, uint32_t wide_bits,
+                                       const MmaParams& p, int m_first, bool n_ok, float* yrow,
+                                       unsigned long long& npos, bool& bad) {
+  float sc[32];
 #pragma unroll
-  for (int j = 0; j < 16; j += 2) {
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(rs[j]), "=d"(rs[j + 1]) : "r"(rs_addr + 8u * j));
+  for (int j = 0; j < 32; j += 4) {
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(sc[j]), "=f"(sc[j + 1]), "=f"(sc[j + 2]), "=f"(sc[j + 3])
+                 : "r"(sc_addr + 4u * j));
   }
+  const int nvalid = min(16, p.M - m_first);  // rows of this chunk inside Y
   float y[16];
-  unsigned cnt = 0;
+  uint32_t negbits = 0;
   float mx = 0.f;
+  const float alpha = p.use_alpha ? p.alpha : 1.f;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-#ifdef TG_EPI_FAST
-    float v = __fmaf_rn(static_cast<float>(tot[j]), static_cast<float>(fabs(rs[j])), static_cast<float>(bn));
-#else
-    float v = static_cast<float>(fma(static_cast<double>(tot[j]), fabs(rs[j]), bn));
-#endif
-    const bool neg = p.use_alpha && !(v > 0.f);
-    const bool live = n_ok && (m_first + j) < p.M;
-    cnt += (neg && live && (rs[j] >= 0.0 || p.fix_var < 0)) ? 1u : 0u;
-    y[j] = neg ? p.alpha * v : v;
-    mx = fmaxf(mx, live ? fabsf(y[j]) : 0.f);
+    const int lo = int(uint32_t(tot[j]) & 0xFFFFFFu);
+    const int hi = int(tot[j] >> 24);
+    const float v = __fmaf_rn(float(hi), sc[2 * j + 1], __fmaf_rn(float(lo), sc[2 * j], bf));
+    const bool neg = !(v > 0.f);
+    negbits |= uint32_t(neg) << j;
+    y[j] = neg ? alpha * v : v;  // alpha = 1 without PReLU: y = v exactly
+    mx = fmaxf(mx, fabsf(y[j]));  // padded rows / columns are exactly b or 0: finite
   }
-  bad |= !(mx <= 3.402823466e38f);
+  // Rows whose scale leaves the fp32 range and have no exact-order fix-up: redo in
+  // full-range fp64, behind a branch that the common path never takes, so the
+  // XU-class fp64 conversions are not issued (not even predicated off).
+  const bool fix = p.fix_var >= 0;
+  if (!fix && wide_bits) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (((wide_bits >> j) & 1u) && j < nvalid) {
+        float v =
+            static_cast<float>(fma(static_cast<double>(tot[j]), fabs(__ldg(p.rscale + m_first + j)), double(bf)));
+        v = (p.use_alpha && !(v > 0.f)) ? p.alpha * v : v;
+        mx = fmaxf(mx, fabsf(v));
+        y[j] = v;
+      }
+    }
+  }
   if (!n_ok) return;
-  npos += cnt;
-#ifdef TG_EPI_NOSTORE
-  if (y[0] == 123.f && y[15] == 7.f) yrow[0] = y[3];
-  return;
-#endif
-  if (m_first + 16 <= p.M) {
+  bad |= !(mx <= 3.402823466e38f);
+  const uint32_t live = nvalid >= 16 ? 0xFFFFu : (nvalid > 0 ? (1u << nvalid) - 1u : 0u);
+  // the reference's `mults`: #(y <= 0) with PReLU; wide rows are counted by the fix-up
+  if (p.use_alpha) npos += __popc(negbits & live & ~(fix ? wide_bits : 0u));
+  if (nvalid >= 16) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) yrow[int64_t(j) * p.ldy] = y[j];
   } else {
 #pragma unroll
     for (int j = 0; j < 16; ++j)
-      if (m_first + j < p.M) yrow[int64_t(j) * p.ldy] = y[j];
+      if (j < nvalid) yrow[int64_t(j) * p.ldy] = y[j];
   }
 }
 
@@ -379,7 +526,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
   uint64_t* tempty = tfull + 2;             // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int32_t* last_flag = reinterpret_cast<int32_t*>(tmem_slot + 1);
-  // [80] row scales of the current unit (16-byte aligned for ld.shared.v2.f64), then [4] wide-row masks
+  // [80] float2 row scales {2^-s, 2^(24-s)} of the current unit (16-byte aligned), then [4] wide-row masks
   double* rs_s = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(tmem_slot + 2) + 15) & ~uintptr_t(15));
 
   const int warp = threadIdx.x >> 5;
@@ -387,6 +534,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
   const int crank = CS > 1 ? int(cluster_ctarank()) : 0;
   const int cid = int(blockIdx.x) / CS, ncl = int(gridDim.x) / CS;
   if (threadIdx.x == 0) TG_STAMP(7, 0);
+  if (threadIdx.x == 0) TG_GT(2);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -415,6 +563,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
   // Programmatic dependent launch: everything above overlapped the X split; its
   // limbs and row scales are read below this point.
   grid_dep_wait();
+  if (threadIdx.x == 0) TG_GT(3);
 
   if (warp == 0) {
     // ---------------- producer of the X limbs (TMA 2D, multicast to the cluster)
@@ -505,9 +654,11 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
           if (CS == 1) mma_commit(&empty[s]);
           else mma_commit_mc(&empty[s], CMASK);
           TG_STAMP(3, it);
+          if (it == 0) TG_GT(4);
         }
         mma_commit(&tfull[acc]);
       }
+      TG_GT(5);
     }
   } else if (warp < 6) {
     // ---------------- decoders (warps 2..5): packed smem -> decoded W^T rows in TMEM.
@@ -580,6 +731,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
     const int et = threadIdx.x - 32 * C::EPI_WARP0;  // 0..ET-1
     const int half = (warp - C::EPI_WARP0) >> 2;
     const uint32_t rs_addr = smem_u32(rs_s);
+    float2* sc_s = reinterpret_cast<float2*>(rs_s);
     uint32_t* wmask = reinterpret_cast<uint32_t*>(rs_s + 80);  // [4] wide-row bits of the unit
     bool any_bad = false;
     unsigned long long npos = 0;
@@ -593,12 +745,11 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
       const int n = n0 + q * 32 + lane;
       const bool n_ok = n < p.N;
       const float bf = (n_ok && p.bias) ? __ldg(p.bias + n) : 0.f;
-      const double bn = double(bf);
       // stage the unit's row scales (and which rows are "wide") in shared memory
       named_bar_sync(1, ET);  // previous unit is done with rs_s / wmask
       {
         const double rs = et < MT ? __ldcg(p.rscale + m0 + et) : 0.0;
-        if (et < MT) rs_s[et] = rs;
+        if (et < MT) sc_s[et] = make_float2(float(fabs(rs)), float(fabs(rs) * 16777216.0));
         const uint32_t wbits = __ballot_sync(0xffffffffu, rs < 0.0);
         if (lane == 0 && (et >> 5) < 4) wmask[et >> 5] = wbits;
       }
@@ -611,6 +762,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
       float* yrow = p.Y + int64_t(m0) * p.ldy + n;
 #pragma unroll 1
       for (int mm = 16 * half; mm < MT; mm += 32) {
+        if (et == 0 && lu == 0) TG_STAMP(7, 200 + mm / 16);
         uint32_t r0[16], r1[16], r2[16];
 #ifdef TG_EPI_NOLDTM
 #pragma unroll
@@ -628,8 +780,11 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
           tot[j] = (static_cast<long long>(static_cast<int>(r0[j])) << 16) +
                    (static_cast<long long>(static_cast<int>(r1[j])) << 8) +
                    static_cast<long long>(static_cast<int>(r2[j]));
+        if (et == 0 && lu == 0) TG_STAMP(7, 220 + mm / 16);
         if (p.splits == 1) {
-          emit16(tot, rs_addr + uint32_t(mm) * 8u, bn, p, m0 + mm, n_ok, yrow + int64_t(mm) * p.ldy, npos, any_bad);
+          emit16(tot, rs_addr + uint32_t(mm) * 8u, bf, (wmask[mm >> 5] >> (mm & 31)) & 0xFFFFu, p, m0 + mm, n_ok,
+                 yrow + int64_t(mm) * p.ldy, npos, any_bad);
+          if (et == 0 && lu == 0) TG_STAMP(7, 240 + mm / 16);
         } else if (!ghost) {
           long long* dst = p.part + (int64_t(split) * p.M_pad + m0 + mm) * p.N_pad + n;
 #pragma unroll
@@ -669,8 +824,8 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
 #pragma unroll
               for (int j = 0; j < 16; ++j) tot[j] += __ldcg(s2 + int64_t(j) * p.N_pad);
             }
-            emit16(tot, rs_addr + uint32_t(j0) * 8u, bn, p, m0 + j0, n_ok, yrow + int64_t(j0) * p.ldy, npos,
-                   any_bad);
+            emit16(tot, rs_addr + uint32_t(j0) * 8u, bf, (wmask[j0 >> 5] >> (j0 & 31)) & 0xFFFFu, p, m0 + j0, n_ok,
+                   yrow + int64_t(j0) * p.ldy, npos, any_bad);
           }
         }
         named_bar_sync(1, ET);  // last_flag is reused by the next unit
@@ -698,6 +853,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
       }
     }
     if (et == 0) TG_STAMP(7, 3 + 2 * (lu - 1));
+    if (et == 0) TG_GT(6);
     if (p.flags) {
       if (__any_sync(0xffffffffu, any_bad) && lane == 0) atomicOr(&p.flags->nonfinite_output, 1);
       for (int o = 16; o; o >>= 1) npos += __shfl_xor_sync(0xffffffffu, npos, o);
@@ -714,6 +870,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
     tmem_dealloc<C::TMEM_COLS>(tmem_base);
   }
   if (threadIdx.x == 0) TG_STAMP(7, 500);
+  if (threadIdx.x == 0) TG_GT(7);
 }
 
 // ------------------------------------------------------------------ pack
@@ -949,6 +1106,24 @@ int run_xsplit(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size
   int8_t* limbs = reinterpret_cast<int8_t*>(base);
   double* rscale = reinterpret_cast<double*>(base + L.off_rscale);
   cudaError_t e = cudaSuccess;
+  // register-resident kernel: one pass over the row when K_pad <= THREADS * EPT
+  const unsigned grid = unsigned(L.M_pad);
+#define TG_XS_REG(T, E)                                                                                       \
+  if (L.K_pad <= int64_t(T) * (E)) {                                                                           \
+    tg_xsplit_reg_kernel<T, E><<<grid, T, 0, st>>>(X, M, K, ldx, limbs, rscale, L.M_pad, L.K_pad, flags);  \
+    return check_launch("tg_xsplit_reg_kernel");                                                               \
+  }
+  if (L.M_pad <= 4 * num_sms()) {  // few rows: wide CTAs so the whole GPU has loads in flight
+    TG_XS_REG(1024, 4)
+    TG_XS_REG(1024, 8)
+    TG_XS_REG(1024, 16)
+  } else {
+    TG_XS_REG(256, 16)
+    TG_XS_REG(256, 32)
+    TG_XS_REG(512, 32)
+  }
+  TG_XS_REG(1024, 32)
+#undef TG_XS_REG
   if (K <= XS_SMEM_MAX_K) {
     const size_t smem = size_t(round_up(K, 4)) * sizeof(float);
     static bool attr = false;
@@ -1134,5 +1309,16 @@ int run_unpack_dense(const uint32_t* tiles, int64_t K, int64_t N, int8_t* W, cud
 #ifdef TG_TRACE
 extern "C" int tg_debug_trace(unsigned long long* host_out) {
   return cudaMemcpyFromSymbol(host_out, tg::g_tg_trace, sizeof(tg::g_tg_trace)) == cudaSuccess ? 0 : 3;
+}
+extern "C" int tg_debug_gt(unsigned long long* host_out, int reset) {
+  if (reset) {
+    unsigned long long init[16][2];
+    for (int i = 0; i < 16; ++i) {
+      init[i][0] = ~0ull;
+      init[i][1] = 0;
+    }
+    return cudaMemcpyToSymbol(tg::g_tg_gt, init, sizeof(init)) == cudaSuccess ? 0 : 3;
+  }
+  return cudaMemcpyFromSymbol(host_out, tg::g_tg_gt, sizeof(tg::g_tg_gt)) == cudaSuccess ? 0 : 3;
 }
 #endif

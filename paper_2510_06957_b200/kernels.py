@@ -282,6 +282,25 @@ class GemmRunner:
                      _p(f.device("col_segment_ptr")), N, b, y, N, order, self.use_alpha, self.alpha, _p(ws),
                      ws.numel(), fl, st)
 
+    def capture(self, warmup: bool = True) -> "torch.cuda.CUDAGraph":
+        """Capture ``launch()`` (X split + tile MMA, or the gather walk) into a CUDA
+        graph: one host launch per replay, no host gaps between the kernels
+        (the tensor-core pair keeps its programmatic-dependent-launch overlap).
+        Replays reuse this runner's buffers (x, y, workspace): refresh x in place."""
+        if self._ws is None:
+            self.pin_workspace()
+        s = torch.cuda.Stream(device=self.x.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            if warmup:
+                self.launch()  # initialises the library's one-time state outside capture
+            s.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                self.launch()
+        torch.cuda.current_stream().wait_stream(s)
+        return g
+
     def pin_workspace(self) -> None:
         """Give this runner a private workspace (needed for graph capture / concurrent replays)."""
         self._ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, device=self.x.device)
