@@ -30,6 +30,23 @@ def _is_tensor(v) -> bool:
     return isinstance(v, torch.Tensor)
 
 
+def _to_host(d: torch.Tensor, extra: torch.Tensor | None = None):
+    """Device -> host through pinned memory (one stream-ordered async copy, one
+    synchronisation); ``extra`` (a small status tensor) rides along and is
+    returned too.  Pinned blocks come from torch's caching host allocator."""
+    if not d.is_cuda:
+        h = d.numpy()
+        return (h, extra.cpu().numpy()) if extra is not None else h
+    h = torch.empty(d.shape, dtype=d.dtype, pin_memory=True)
+    h.copy_(d, non_blocking=True)
+    he = None
+    if extra is not None:
+        he = torch.empty(extra.shape, dtype=extra.dtype, pin_memory=True)
+        he.copy_(extra, non_blocking=True)
+    torch.cuda.current_stream(d.device).synchronize()
+    return (h.numpy(), he.numpy()) if extra is not None else h.numpy()
+
+
 class _Dual:
     """Host/device pair with lazy, cached transfers."""
 
@@ -41,7 +58,7 @@ class _Dual:
 
     def host(self) -> np.ndarray:
         if self._h is None:
-            self._h = self._d.detach().cpu().numpy()
+            self._h = _to_host(self._d.detach())
         return self._h
 
     def dev(self) -> torch.Tensor:
@@ -152,8 +169,17 @@ class DenseMatrix:
 
     @property
     def values(self) -> np.ndarray:
+        v = self._v
+        if v._h is None and not self._checked and self._flags is not None and v._d is not None and v._d.is_cuda:
+            # fetch Y and the kernel's status words with one synchronisation
+            h, f = _to_host(v._d.detach(), self._flags)
+            if int(f[1]) != 0:
+                raise ParameterError("dense matrix contains non-finite values")
+            self._checked = True
+            v._h = h
+            return h
         self.check()
-        return self._v.host()
+        return v.host()
 
     @property
     def device_values(self) -> torch.Tensor:

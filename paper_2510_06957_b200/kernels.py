@@ -140,11 +140,21 @@ class PaddedInput:
 
 
 def pad_input(X) -> PaddedInput:
-    """simd.py:72-75, on the device."""
+    """simd.py:72-75, on the device.  A host input is copied straight into the
+    padded device buffer (one strided, stream-ordered copy; asynchronous from
+    pinned memory) instead of uploading X and copying it again."""
     X = as_dense(X)
-    x = X.device_values
-    xp = torch.zeros((x.shape[0], x.shape[1] + 1), dtype=torch.float32, device=x.device)
-    xp[:, :-1] = x
+    v = X._v
+    if v._d is not None and v._d.is_cuda:
+        x = v._d
+        xp = torch.empty((x.shape[0], x.shape[1] + 1), dtype=torch.float32, device=x.device)
+        xp[:, :-1].copy_(x)
+    else:
+        src = v._d if v._d is not None else torch.from_numpy(np.ascontiguousarray(v._h))
+        M, K = int(src.shape[0]), int(src.shape[1])
+        xp = torch.empty((M, K + 1), dtype=torch.float32, device=_device())
+        xp[:, :-1].copy_(src, non_blocking=src.is_pinned())
+    xp[:, -1].zero_()
     return PaddedInput._trusted(xp)
 
 
