@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define TG_ABI_VERSION 1
+#define TG_ABI_VERSION 2
 
 typedef enum {
   TG_OK = 0,
@@ -49,6 +49,7 @@ typedef enum {
 #define TG_FMT_TCSC 0                /* tcsc.py:35 Tcsc                      */
 #define TG_FMT_BLOCKED 1             /* variants.py:86 BlockedTcsc           */
 #define TG_FMT_INTERLEAVED_BLOCKED 2 /* variants.py:251 InterleavedBlockedTcsc */
+#define TG_FMT_SYMMETRIC 3           /* variants.py:540 SymmetricInterleavedTcsc */
 
 /* Orders of the interleaved-blocked gather kernel. */
 #define TG_ORDER_INTERLEAVED_BLOCKED 0 /* kernels/scalar.py:397-485 */
@@ -59,7 +60,8 @@ typedef struct {
   int32_t bad_input;           /* bit0: W entry outside {-1,0,1}; bit1: index out of range; bit2: non-finite X */
   int32_t nonfinite_output;    /* 1 if any produced Y entry is inf/nan (dense.py:77 DenseMatrix check) */
   uint64_t nonpositive_outputs;/* #(y <= 0) before PReLU: the reference's `mults` counter (simd.py:410-417) */
-  int32_t corrupt;             /* bit0: duplicate (row, col); bit1: cell in both sign arrays (tcsc.py:95-114) */
+  int32_t corrupt;             /* bit0: duplicate (row, col); bit1: cell in both sign arrays (tcsc.py:95-114);
+                                  bit2: a packed code >= 243 (variants.py:505-507, InvalidCodeError) */
   int32_t _pad;
 } tg_device_flags;
 
@@ -100,6 +102,15 @@ int tg_build_fill_blocked(const void* ws, int64_t K, int64_t N, int64_t B, int32
 int tg_build_fill_interleaved_blocked(const void* ws, int64_t K, int64_t N, int64_t B, int g, int symmetric,
                                       int32_t* all_indices, int32_t* col_segment_ptr /* 3*nb*N+1 */,
                                       void* stream);
+/* variants.py:582-631 symmetric_from_dense(W, g): kind TG_FMT_SYMMETRIC in
+ * tg_build_count (B ignored), then this fill; n_indices = sizes.n_indices. */
+int tg_build_fill_symmetric(const void* ws, int64_t K, int64_t N, int g, int32_t* indices,
+                            int32_t* col_ptr /* N+1 */, int64_t n_indices, void* stream);
+/* variants.py:515-521 compressed_from_dense(W): codes is N x ceil(K/5) uint8
+ * (column-major packed, 5 base-3 digits per byte).  Validates W; synchronises. */
+int tg_build_compressed(const int8_t* W, int64_t K, int64_t N, int64_t ldw, uint8_t* codes, void* stream);
+/* Sets flags->corrupt bit2 if any code is >= 243 (CompressedTcsc.__post_init__, variants.py:503-507). */
+int tg_codes_check(const uint8_t* codes, int64_t count, tg_device_flags* flags, void* stream);
 
 /* ------------------------------------------------------------------ ternary tiles
  * GPU-native re-encoding of any of the formats above for the dense-decode
@@ -118,6 +129,9 @@ int tg_tiles_from_blocked(const int32_t* col_start_pos, const int32_t* row_index
 int tg_tiles_from_interleaved_blocked(const int32_t* all_indices, const int32_t* col_segment_ptr, int64_t K,
                                       int64_t N, int64_t B, int g, uint32_t* tiles, tg_device_flags* flags,
                                       void* stream);
+int tg_tiles_from_symmetric(const int32_t* indices, const int32_t* col_ptr, int64_t K, int64_t N, int g,
+                            uint32_t* tiles, tg_device_flags* flags, void* stream);
+int tg_tiles_from_compressed(const uint8_t* codes, int64_t K, int64_t N, uint32_t* tiles, void* stream);
 /* Decode tiles back to dense int8 W (K x N, ld = N): tcsc.py:95 tcsc_to_dense. */
 int tg_tiles_to_dense(const uint32_t* tiles, int64_t K, int64_t N, int8_t* W, void* stream);
 
@@ -148,6 +162,17 @@ int tg_gemm_interleaved_blocked(const float* X, int64_t M, int64_t K, int64_t ld
                                 const int32_t* all_indices, const int32_t* col_segment_ptr, int64_t N,
                                 const float* bias, float* Y, int64_t ldy, int order, int use_alpha, float alpha,
                                 void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream);
+/* gemm_vertical (order 0, kernels/simd.py:98-188) and gemm_horizontal (order 1,
+ * kernels/simd.py:196-274) over a SymmetricInterleavedTcsc; X padded (ldx = K+1). */
+#define TG_ORDER_VERTICAL 0
+#define TG_ORDER_HORIZONTAL 1
+int tg_gemm_symmetric(const float* X, int64_t M, int64_t K, int64_t ldx, int g, const int32_t* indices,
+                      const int32_t* col_ptr, int64_t N, const float* bias, float* Y, int64_t ldy, int order,
+                      int use_alpha, float alpha, void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream);
+/* gemm_compressed, kernels/scalar.py:561-602 (codes N x ceil(K/5)). */
+int tg_gemm_compressed(const float* X, int64_t M, int64_t K, int64_t ldx, const uint8_t* codes, int64_t N,
+                       const float* bias, float* Y, int64_t ldy, void* ws, size_t ws_bytes, tg_device_flags* flags,
+                       void* stream);
 
 /* Reference kernel whose fp32 operation order a gather walk reproduces. */
 #define TG_VARIANT_BASE 0               /* kernels/scalar.py:109-148 */
@@ -155,12 +180,17 @@ int tg_gemm_interleaved_blocked(const float* X, int64_t M, int64_t K, int64_t ld
 #define TG_VARIANT_INTERLEAVED_BLOCKED 2 /* kernels/scalar.py:397-511 */
 #define TG_VARIANT_VECTORIZED_OPTIMAL 3 /* kernels/simd.py:282-449  */
 #define TG_VARIANT_UNROLLED 4           /* kernels/scalar.py:156-278 */
+#define TG_VARIANT_VERTICAL 5           /* kernels/simd.py:98-188    */
+#define TG_VARIANT_HORIZONTAL 6         /* kernels/simd.py:196-274   */
+#define TG_VARIANT_COMPRESSED 7         /* kernels/scalar.py:561-602 */
 
 /* The format a tensor-core call was derived from, for the exact-order fix-up
  * of rows the fixed-point limbs cannot carry (see tg_gemm_tiles).
  *   BASE / UNROLLED: a0..a3 = col_start_pos, row_index_pos, col_start_neg, row_index_neg
  *   BLOCKED:         same four arrays of the blocked format, plus B
- *   INTERLEAVED_BLOCKED / VECTORIZED_OPTIMAL: a0 = col_segment_ptr, a1 = all_indices, B, g */
+ *   INTERLEAVED_BLOCKED / VECTORIZED_OPTIMAL: a0 = col_segment_ptr, a1 = all_indices, B, g
+ *   VERTICAL / HORIZONTAL: a0 = col_ptr, a1 = indices, g
+ *   COMPRESSED:      codes */
 typedef struct {
   int32_t variant;
   int32_t g;
@@ -171,6 +201,7 @@ typedef struct {
   const int32_t* a1;
   const int32_t* a2;
   const int32_t* a3;
+  const uint8_t* codes;
 } tg_format_ref;
 
 /* Dense-decode tensor-core path.

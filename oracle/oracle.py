@@ -30,6 +30,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtg_oracle.so")
 
 KIND_BASE, KIND_UNROLLED, KIND_BLOCKED, KIND_IB, KIND_OPTIMAL = 0, 1, 2, 3, 4
+KIND_VERTICAL, KIND_HORIZONTAL, KIND_COMPRESSED = 5, 6, 7
 
 _lib = None
 
@@ -52,6 +53,9 @@ def lib() -> ctypes.CDLL:
         L.tgo_blocked_from_dense.argtypes = [P, I64, I64, I64, P, P, P, P]
         L.tgo_interleaved_blocked_from_dense.argtypes = [P, I64, I64, I64, I, I, P, P]
         L.tgo_interleaved_blocked_from_dense.restype = I64
+        L.tgo_symmetric_from_dense.argtypes = [P, I64, I64, I, P, P]
+        L.tgo_symmetric_from_dense.restype = I64
+        L.tgo_compressed_from_dense.argtypes = [P, I64, I64, P]
         L.tgo_run_threaded.argtypes = [I, I, P, I64, I64, P, P, P, P, I64, I, I, I, P, I64, I, F, P]
         L.tgo_run_threaded.restype = I
         _lib = L
@@ -112,6 +116,27 @@ def interleaved_blocked_from_dense(W, B=None, g: int = 2, symmetric_cols: bool =
     ai = np.empty(int(n), np.int32)
     lib().tgo_interleaved_blocked_from_dense(_ptr(w), K, N, B, g, int(symmetric_cols), _ptr(ai), _ptr(ptr))
     return dict(K=K, N=N, B=B, g=g, all_indices=ai, col_segment_ptr=ptr, symmetric_groups=bool(symmetric_cols))
+
+
+def symmetric_from_dense(W, g: int = 2) -> dict:
+    """variants.py:582-631."""
+    w = _w(W)
+    K, N = w.shape
+    assert N % 4 == 0
+    ptr = np.zeros(N + 1, np.int32)
+    n = lib().tgo_symmetric_from_dense(_ptr(w), K, N, g, None, _ptr(ptr))
+    idx = np.empty(int(n), np.int32)
+    lib().tgo_symmetric_from_dense(_ptr(w), K, N, g, _ptr(idx), _ptr(ptr))
+    return dict(K=K, N=N, g=g, indices=idx, col_ptr=ptr)
+
+
+def compressed_from_dense(W) -> dict:
+    """variants.py:515-521."""
+    w = _w(W)
+    K, N = w.shape
+    codes = np.empty((N, (K + 4) // 5), np.uint8)
+    lib().tgo_compressed_from_dense(_ptr(w), K, N, _ptr(codes))
+    return dict(K=K, N=N, codes=codes)
 
 
 # ---------------------------------------------------------------- inputs
@@ -185,6 +210,30 @@ def gemm_vectorized_optimal(Xp, t: dict, b, alpha=None, threads=1):
     nb = -(-t["K"] // t["B"])
     return _run(KIND_OPTIMAL, Xp, [t["all_indices"], t["col_segment_ptr"]], t["N"], b, threads, nb=nb, g=t["g"],
                 alpha=alpha)
+
+
+def gemm_vertical(Xp, t: dict, b, alpha=None, threads=1):
+    """kernels/simd.py:98-188; Xp is the padded M x (K+1) input."""
+    return _run(KIND_VERTICAL, Xp, [t["indices"], t["col_ptr"]], t["N"], b, threads, g=t["g"], alpha=alpha)
+
+
+def gemm_horizontal(Xp, t: dict, b, alpha=None, threads=1):
+    """kernels/simd.py:196-274."""
+    return _run(KIND_HORIZONTAL, Xp, [t["indices"], t["col_ptr"]], t["N"], b, threads, g=t["g"], alpha=alpha)
+
+
+def gemm_compressed(X, t: dict, b, threads=1):
+    """kernels/scalar.py:561-602."""
+    codes = np.ascontiguousarray(t["codes"], dtype=np.uint8)
+    x = np.ascontiguousarray(X, dtype=np.float32)
+    M, ldx = x.shape
+    bb = np.ascontiguousarray(b, dtype=np.float32)
+    y = np.empty((M, t["N"]), np.float32)
+    rc = lib().tgo_run_threaded(KIND_COMPRESSED, int(threads), _ptr(x), M, ldx, _ptr(codes), None, None, None,
+                                codes.shape[1], 1, 1, 1, _ptr(bb), t["N"], 0, 0.0, _ptr(y))
+    if rc != 0:
+        raise RuntimeError("tgo_run_threaded failed")
+    return y
 
 
 # ---------------------------------------------------------------- parity predicates

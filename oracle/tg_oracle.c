@@ -155,6 +155,84 @@ i64 tgo_interleaved_blocked_from_dense(const int8_t* W, i64 K, i64 N, i64 B, int
   return off;
 }
 
+/* variants.py:582-631 symmetric_from_dense.  One stream per column: runs of g
+ * positives then g negatives (ascending rows), every stream of a 4-column group
+ * holds `pairs` index pairs, pairs = the group's max(max(#pos, #neg)) rounded
+ * up to lcm(4, g) (0 for an all-zero group); the deficit is padded with K.
+ * col_ptr has N+1 entries.  Returns len(indices); pass idx = NULL to size. */
+static i64 lcm4(i64 g) {
+  i64 a = 4, b = g;
+  while (b) {
+    const i64 t = a % b;
+    a = b;
+    b = t;
+  }
+  return 4 / a * g;
+}
+i64 tgo_symmetric_from_dense(const int8_t* W, i64 K, i64 N, int g, i32* idx, i32* col_ptr) {
+  const i64 quantum = lcm4(g);
+  i32* pos = (i32*)malloc(sizeof(i32) * (size_t)(K > 0 ? K : 1));
+  i32* neg = (i32*)malloc(sizeof(i32) * (size_t)(K > 0 ? K : 1));
+  i64 off = 0;
+  col_ptr[0] = 0;
+  for (i64 n0 = 0; n0 < N; n0 += 4) {
+    i64 need = 0;
+    for (int c = 0; c < 4; ++c) {
+      i64 p = 0, q = 0;
+      for (i64 k = 0; k < K; ++k) {
+        const int8_t v = W[k * N + n0 + c];
+        p += (v == 1);
+        q += (v == -1);
+      }
+      const i64 m = p > q ? p : q;
+      need = m > need ? m : need;
+    }
+    const i64 pairs = need ? (need + quantum - 1) / quantum * quantum : 0;
+    for (int c = 0; c < 4; ++c) {
+      i64 p = 0, q = 0;
+      for (i64 k = 0; k < K; ++k) {
+        const int8_t v = W[k * N + n0 + c];
+        if (v == 1) pos[p++] = (i32)k;
+        else if (v == -1) neg[q++] = (i32)k;
+      }
+      for (i64 run = 0; run < pairs / g; ++run) {
+        for (int u = 0; u < g; ++u) {
+          const i64 t = run * g + u;
+          if (idx) idx[off] = t < p ? pos[t] : (i32)K;
+          ++off;
+        }
+        for (int u = 0; u < g; ++u) {
+          const i64 t = run * g + u;
+          if (idx) idx[off] = t < q ? neg[t] : (i32)K;
+          ++off;
+        }
+      }
+      col_ptr[n0 + c + 1] = (i32)off;
+    }
+  }
+  free(pos);
+  free(neg);
+  return off;
+}
+
+/* variants.py:451-532 compressed_from_dense: codes[n][gi] = sum_i (w(5gi+i, n) + 1) 3^i,
+ * columns zero-padded to a multiple of 5. */
+void tgo_compressed_from_dense(const int8_t* W, i64 K, i64 N, uint8_t* codes) {
+  const i64 G = (K + 4) / 5;
+  for (i64 n = 0; n < N; ++n) {
+    for (i64 gi = 0; gi < G; ++gi) {
+      int code = 0, p3 = 1;
+      for (int i = 0; i < 5; ++i) {
+        const i64 k = 5 * gi + i;
+        const int v = k < K ? W[k * N + n] : 0;
+        code += (v + 1) * p3;
+        p3 *= 3;
+      }
+      codes[n * G + gi] = (uint8_t)code;
+    }
+  }
+}
+
 /* ------------------------------------------------------------------ kernels
  * X is M x ldx row-major (ldx = K, or K+1 for a PaddedInput whose slot K is 0),
  * Y is M x N.  Column range [n_lo, n_hi). */
@@ -320,10 +398,79 @@ void tgo_gemm_vectorized_optimal(const float* Xp, i64 M, i64 ldx, const i32* ai,
   }
 }
 
+/* kernels/simd.py:98-188 gemm_vertical over a SymmetricInterleavedTcsc: per
+ * column, positive-run and negative-run sums (run parity of the stream
+ * position t: (t / g) & 1) and y = (b + p) - q, PReLU.  n_lo, n_hi multiples of 4. */
+void tgo_gemm_vertical(const float* Xp, i64 M, i64 ldx, const i32* idx, const i32* col_ptr, int g, const float* bias,
+                       i64 N, int use_alpha, float alpha, float* Y, i64 n_lo, i64 n_hi) {
+  for (i64 m = 0; m < M; ++m) {
+    const float* x = Xp + m * ldx;
+    for (i64 n = n_lo; n < n_hi; ++n) {
+      const i32 s = col_ptr[n], len = col_ptr[n + 1] - col_ptr[n];
+      float p = 0.0f, q = 0.0f;
+      for (i32 t = 0; t < len; ++t) {
+        const float v = x[idx[s + t]];
+        if (((t / g) & 1) == 0) p += v;
+        else q += v;
+      }
+      float y = bias[n] + p - q;
+      if (use_alpha && !(y > 0.0f)) y = alpha * y;
+      Y[m * N + n] = y;
+    }
+  }
+}
+
+/* kernels/simd.py:196-274 gemm_horizontal: four lane accumulators take stream
+ * positions t = 0, 1, 2, 3 (mod 4), sign = ((t / g) & 1); y = b + ((a0 + a1) + (a2 + a3)). */
+void tgo_gemm_horizontal(const float* Xp, i64 M, i64 ldx, const i32* idx, const i32* col_ptr, int g,
+                         const float* bias, i64 N, int use_alpha, float alpha, float* Y, i64 n_lo, i64 n_hi) {
+  for (i64 m = 0; m < M; ++m) {
+    const float* x = Xp + m * ldx;
+    for (i64 n = n_lo; n < n_hi; ++n) {
+      const i32 s = col_ptr[n], e = col_ptr[n + 1];
+      float a[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      for (i32 w = s; w < e; w += 4) {
+        const i32 t = w - s;
+        for (int j = 0; j < 4; ++j) {
+          const float v = x[idx[w + j]];
+          if ((((t + j) / g) & 1) == 0) a[j] += v;
+          else a[j] -= v;
+        }
+      }
+      float y = bias[n] + ((a[0] + a[1]) + (a[2] + a[3]));
+      if (use_alpha && !(y > 0.0f)) y = alpha * y;
+      Y[m * N + n] = y;
+    }
+  }
+}
+
+/* kernels/scalar.py:561-602 gemm_compressed: per column, codes in order, the 5
+ * base-3 digits of each code (digit 2 -> +x, 0 -> -x), out = b + acc. */
+void tgo_gemm_compressed(const float* X, i64 M, i64 ldx, const uint8_t* codes, i64 G, const float* bias, i64 N,
+                         float* Y, i64 n_lo, i64 n_hi) {
+  for (i64 m = 0; m < M; ++m) {
+    const float* x = X + m * ldx;
+    for (i64 n = n_lo; n < n_hi; ++n) {
+      float acc = 0.0f;
+      for (i64 gi = 0; gi < G; ++gi) {
+        int code = codes[n * G + gi];
+        for (int t = 0; t < 5; ++t) {
+          const int d = code % 3 - 1;
+          code /= 3;
+          if (d > 0) acc += x[5 * gi + t];
+          else if (d < 0) acc -= x[5 * gi + t];
+        }
+      }
+      Y[m * N + n] = bias[n] + acc;
+    }
+  }
+}
+
 /* ------------------------------------------------------------------ threaded driver
  * Runs one of the kernels above over `threads` disjoint column ranges
  * (multiples of 4) with pthreads.  kind: 0 base, 1 unrolled, 2 blocked,
- * 3 interleaved_blocked, 4 vectorized_optimal. */
+ * 3 interleaved_blocked, 4 vectorized_optimal, 5 vertical (a0 = indices,
+ * a1 = col_ptr), 6 horizontal, 7 compressed (a0 = codes, nb = groups per column). */
 typedef struct {
   int kind;
   const float* X;
@@ -353,6 +500,17 @@ static void* tgo_worker(void* arg) {
       break;
     case 3:
       tgo_gemm_interleaved_blocked(j->X, j->M, j->ldx, j->a0, j->a1, j->nb, j->g, j->bias, j->N, j->Y, j->lo, j->hi);
+      break;
+    case 5:
+      tgo_gemm_vertical(j->X, j->M, j->ldx, j->a0, j->a1, j->g, j->bias, j->N, j->use_alpha, j->alpha, j->Y, j->lo,
+                        j->hi);
+      break;
+    case 6:
+      tgo_gemm_horizontal(j->X, j->M, j->ldx, j->a0, j->a1, j->g, j->bias, j->N, j->use_alpha, j->alpha, j->Y,
+                          j->lo, j->hi);
+      break;
+    case 7:
+      tgo_gemm_compressed(j->X, j->M, j->ldx, (const uint8_t*)j->a0, j->nb, j->bias, j->N, j->Y, j->lo, j->hi);
       break;
     default:
       tgo_gemm_vectorized_optimal(j->X, j->M, j->ldx, j->a0, j->a1, j->nb, j->g, j->bias, j->N, j->use_alpha,

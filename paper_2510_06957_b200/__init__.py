@@ -10,10 +10,19 @@ GEMM variants and the variant registry — backed by hand-written sm_100a CUDA
 from .dense import BiasVector, DenseMatrix, TernaryDense, oracle_gemm, prelu
 from .errors import CorruptionError, InvalidCodeError, ParameterError, ParseError, VerificationError
 from .formats import (
+    CODE_COUNT,
+    DECODE_TABLE,
+    PACK_WIDTH,
     BlockedTcsc,
+    CompressedTcsc,
     InterleavedBlockedTcsc,
+    SymmetricInterleavedTcsc,
     Tcsc,
     blocked_from_dense,
+    compress5,
+    compressed_from_dense,
+    decompress5,
+    symmetric_from_dense,
     format_bytes,
     interleaved_blocked_from_dense,
     resolve_block_size,
@@ -35,9 +44,12 @@ from .kernels import (
     VariantSpec,
     gemm_base,
     gemm_blocked,
+    gemm_compressed,
+    gemm_horizontal,
     gemm_interleaved_blocked,
     gemm_unrolled,
     gemm_vectorized_optimal,
+    gemm_vertical,
     get_variant,
     pad_input,
     run_variant,
@@ -46,6 +58,9 @@ from .kernels import (
 __version__ = "0.1.0"
 
 __all__ = [
+    "CODE_COUNT", "CompressedTcsc", "DECODE_TABLE", "PACK_WIDTH", "SymmetricInterleavedTcsc", "compress5",
+    "compressed_from_dense", "decompress5", "gemm_compressed", "gemm_horizontal", "gemm_vertical",
+    "symmetric_from_dense",
     "BiasVector", "BlockedTcsc", "CorruptionError", "DEFAULT_ALPHA", "DenseMatrix", "GemmConfig", "GemmRunner",
     "InterleavedBlockedTcsc", "InvalidCodeError", "OpCount", "PaddedInput", "ParameterError", "ParseError",
     "SCALAR_TAGS", "SIMD_TAGS", "Tcsc", "TernaryDense", "VARIANTS", "VariantSpec", "VerificationError",

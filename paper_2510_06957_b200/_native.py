@@ -31,9 +31,12 @@ TG_ERR_OVERFLOW = 5
 TG_FMT_TCSC = 0
 TG_FMT_BLOCKED = 1
 TG_FMT_INTERLEAVED_BLOCKED = 2
+TG_FMT_SYMMETRIC = 3
 
 TG_ORDER_INTERLEAVED_BLOCKED = 0
 TG_ORDER_VECTORIZED_OPTIMAL = 1
+TG_ORDER_VERTICAL = 0
+TG_ORDER_HORIZONTAL = 1
 
 
 class NativeError(RuntimeError):
@@ -55,6 +58,9 @@ TG_VARIANT_BLOCKED = 1
 TG_VARIANT_INTERLEAVED_BLOCKED = 2
 TG_VARIANT_VECTORIZED_OPTIMAL = 3
 TG_VARIANT_UNROLLED = 4
+TG_VARIANT_VERTICAL = 5
+TG_VARIANT_HORIZONTAL = 6
+TG_VARIANT_COMPRESSED = 7
 
 
 class TgFormatRef(ctypes.Structure):
@@ -68,6 +74,7 @@ class TgFormatRef(ctypes.Structure):
         ("a1", ctypes.c_void_p),
         ("a2", ctypes.c_void_p),
         ("a3", ctypes.c_void_p),
+        ("codes", ctypes.c_void_p),
     ]
 
 
@@ -91,11 +98,16 @@ SIGNATURES: dict[str, tuple] = {
     "tg_build_fill_tcsc": (_I, [_P, _I64, _I64, _P, _P, _P, _P, _P]),
     "tg_build_fill_blocked": (_I, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _P]),
     "tg_build_fill_interleaved_blocked": (_I, [_P, _I64, _I64, _I64, _I, _I, _P, _P, _P]),
+    "tg_build_fill_symmetric": (_I, [_P, _I64, _I64, _I, _P, _P, _I64, _P]),
+    "tg_build_compressed": (_I, [_P, _I64, _I64, _I64, _P, _P]),
+    "tg_codes_check": (_I, [_P, _I64, _P, _P]),
     "tg_tiles_bytes": (_SZ, [_I64, _I64]),
     "tg_tiles_from_dense": (_I, [_P, _I64, _I64, _I64, _P, _P, _P]),
     "tg_tiles_from_tcsc": (_I, [_P, _P, _P, _P, _I64, _I64, _P, _P, _P]),
     "tg_tiles_from_blocked": (_I, [_P, _P, _P, _P, _I64, _I64, _I64, _P, _P, _P]),
     "tg_tiles_from_interleaved_blocked": (_I, [_P, _P, _I64, _I64, _I64, _I, _P, _P, _P]),
+    "tg_tiles_from_symmetric": (_I, [_P, _P, _I64, _I64, _I, _P, _P, _P]),
+    "tg_tiles_from_compressed": (_I, [_P, _I64, _I64, _P, _P]),
     "tg_tiles_to_dense": (_I, [_P, _I64, _I64, _P, _P]),
     "tg_gemm_workspace_bytes": (_SZ, [_I64, _I64, _I64]),
     "tg_gemm_tcsc": (_I, [_P, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _P, _P, _I64, _I, _I, _F, _P, _SZ, _P, _P]),
@@ -107,6 +119,11 @@ SIGNATURES: dict[str, tuple] = {
         _I,
         [_P, _I64, _I64, _I64, _I64, _I, _P, _P, _I64, _P, _P, _I64, _I, _I, _F, _P, _SZ, _P, _P],
     ),
+    "tg_gemm_symmetric": (
+        _I,
+        [_P, _I64, _I64, _I64, _I, _P, _P, _I64, _P, _P, _I64, _I, _I, _F, _P, _SZ, _P, _P],
+    ),
+    "tg_gemm_compressed": (_I, [_P, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _P, _SZ, _P, _P]),
     "tg_gemm_tiles_prepare": (_I, [_P, _I64, _I64, _I64, _P, _SZ, _P, _P]),
     "tg_gemm_tiles_run": (_I, [_P, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _I, _F, _P, _P, _SZ, _P, _P]),
     "tg_gemm_tiles": (_I, [_P, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _I, _F, _P, _P, _SZ, _P, _P]),

@@ -323,6 +323,93 @@ __global__ void fill_dummies_kernel(const int32_t* __restrict__ cellP, const int
   }
 }
 
+// ---- SymmetricInterleavedTcsc (variants.py:540-631): one stream per column,
+// pairs per 4-column group = the group's max(max(p, q)) rounded up to lcm(4, g).
+__device__ __forceinline__ int64_t sym_quantum(int g) {
+  int a = 4, b = g;
+  while (b) {
+    const int t = a % b;
+    a = b;
+    b = t;
+  }
+  return int64_t(4 / a) * g;
+}
+
+__global__ void sym_lengths_kernel(const int32_t* __restrict__ cellP, const int32_t* __restrict__ cellQ, int64_t N,
+                                   int g, int64_t* __restrict__ len) {
+  for (int64_t n = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; n < N; n += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t n0 = n & ~int64_t(3);
+    int64_t need = 0;
+    for (int j = 0; j < 4; ++j) {
+      const int64_t m = max(cellP[n0 + j], cellQ[n0 + j]);
+      need = m > need ? m : need;
+    }
+    const int64_t q = sym_quantum(g);
+    len[n] = need ? 2 * ((need + q - 1) / q * q) : 0;
+  }
+}
+
+__global__ void fill_value_kernel(int32_t* __restrict__ a, int64_t n, int32_t v) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    a[i] = v;
+}
+
+// t-th positive of column n -> s0 + 2g (t / g) + (t % g); t-th negative -> ... + g.
+__global__ void fill_sym_kernel(const uint32_t* __restrict__ P, const uint32_t* __restrict__ Q,
+                                const int32_t* __restrict__ cpP, const int32_t* __restrict__ cpQ,
+                                const int64_t* __restrict__ start, int64_t N, int64_t KW, int g,
+                                int32_t* __restrict__ idx) {
+  const int64_t total = KW * N;
+  for (int64_t id = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; id < total; id += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t w = id / N, n = id % N;
+    const int64_t s0 = start[n];
+#pragma unroll 1
+    for (int sign = 0; sign < 2; ++sign) {
+      uint32_t bits = (sign ? Q : P)[id];
+      int64_t t = (sign ? cpQ : cpP)[id];  // rank of the first set bit in its column
+      while (bits) {
+        const int j = __ffs(bits) - 1;
+        bits &= bits - 1;
+        idx[s0 + 2 * g * (t / g) + (sign ? g : 0) + (t % g)] = int32_t(w * 32 + j);
+        ++t;
+      }
+    }
+  }
+}
+
+// ---- CompressedTcsc (variants.py:451-532): codes[n][gi] = sum_i (w(5gi+i, n) + 1) 3^i.
+// Thread per (gi, n), n fastest so the reads of W rows coalesce.
+__global__ void compress_kernel(const int8_t* __restrict__ W, int64_t K, int64_t N, int64_t ldw, int64_t G,
+                                uint8_t* __restrict__ codes, unsigned long long* __restrict__ bad) {
+  const int64_t total = G * N;
+  for (int64_t id = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; id < total; id += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t gi = id / N, n = id % N;
+    int code = 0, p3 = 1;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const int64_t k = 5 * gi + i;
+      int v = 0;
+      if (k < K) {
+        v = W[k * ldw + n];
+        if (v < -1 || v > 1) {
+          atomicMin(bad, (unsigned long long)(k * N + n));
+          v = 0;
+        }
+      }
+      code += (v + 1) * p3;
+      p3 *= 3;
+    }
+    codes[n * G + gi] = uint8_t(code);
+  }
+}
+
+__global__ void codes_check_kernel(const uint8_t* __restrict__ codes, int64_t n, tg_device_flags* __restrict__ flags) {
+  bool badc = false;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    badc |= codes[i] >= 243;
+  if (__any_sync(0xffffffffu, badc) && (threadIdx.x & 31) == 0) atomicOr(&flags->corrupt, 4);
+}
+
 unsigned grid_for(int64_t work, int threads = 256) {
   const int64_t b = (work + threads - 1) / threads;
   return unsigned(std::max<int64_t>(1, std::min<int64_t>(b, 148 * 64)));
@@ -364,12 +451,15 @@ int tg_build_count(const int8_t* W, int64_t K, int64_t N, int64_t ldw, int kind,
   if (B < 1) return set_error(TG_ERR_PARAM, "block size must be >= 1");
   if (ldw < N) return set_error(TG_ERR_PARAM, "ldw must be >= N");
   if (!W || !ws || !sizes) return set_error(TG_ERR_PARAM, "null pointer");
-  if (kind != TG_FMT_TCSC && kind != TG_FMT_BLOCKED && kind != TG_FMT_INTERLEAVED_BLOCKED)
+  if (kind != TG_FMT_TCSC && kind != TG_FMT_BLOCKED && kind != TG_FMT_INTERLEAVED_BLOCKED &&
+      kind != TG_FMT_SYMMETRIC)
     return set_error(TG_ERR_PARAM, "unknown format kind");
+  if (kind == TG_FMT_SYMMETRIC && (g < 1 || N % 4 != 0))
+    return set_error(TG_ERR_PARAM, g < 1 ? "group size must be >= 1" : "N must be divisible by 4");
   if (kind == TG_FMT_INTERLEAVED_BLOCKED && g < 1) return set_error(TG_ERR_PARAM, "group size must be >= 1");
   if (kind == TG_FMT_INTERLEAVED_BLOCKED && symmetric && N % 4 != 0)
     return set_error(TG_ERR_PARAM, "symmetric groups need N divisible by 4");
-  if (kind == TG_FMT_TCSC) B = K;
+  if (kind == TG_FMT_TCSC || kind == TG_FMT_SYMMETRIC) B = K;
   if (K >= INT32_MAX) return set_error(TG_ERR_OVERFLOW, "K does not fit int32 row indices");
   const Layout Lo = make_layout(K, N, B);
   if (ws_bytes < Lo.total) return set_error(TG_ERR_PARAM, "build workspace too small");
@@ -397,6 +487,9 @@ int tg_build_count(const int8_t* W, int64_t K, int64_t N, int64_t ldw, int kind,
   if (kind == TG_FMT_INTERLEAVED_BLOCKED) {
     ib_lengths_kernel<<<grid_for(Lo.ncell), 256, 0, st>>>(cellP, cellQ, N, Lo.ncell, g, symmetric, scanP);
     rc = run_scan(scanP, Lo.nseg, chunk, st);
+  } else if (kind == TG_FMT_SYMMETRIC) {
+    sym_lengths_kernel<<<grid_for(N), 256, 0, st>>>(cellP, cellQ, N, g, scanP);
+    rc = run_scan(scanP, N, chunk, st);
   } else {
     copy_lengths_kernel<<<grid_for(Lo.ncell), 256, 0, st>>>(cellP, Lo.ncell, scanP);
     copy_lengths_kernel<<<grid_for(Lo.ncell), 256, 0, st>>>(cellQ, Lo.ncell, scanQ);
@@ -412,9 +505,10 @@ int tg_build_count(const int8_t* W, int64_t K, int64_t N, int64_t ldw, int kind,
   int64_t totP = 0, totQ = 0;
   e = cudaMemcpyAsync(&bad_h, bad, sizeof(bad_h), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess)
-    e = cudaMemcpyAsync(&totP, scanP + (kind == TG_FMT_INTERLEAVED_BLOCKED ? Lo.nseg : Lo.ncell), sizeof(int64_t),
-                        cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess && kind != TG_FMT_INTERLEAVED_BLOCKED)
+    e = cudaMemcpyAsync(&totP,
+                        scanP + (kind == TG_FMT_INTERLEAVED_BLOCKED ? Lo.nseg : kind == TG_FMT_SYMMETRIC ? N : Lo.ncell),
+                        sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && kind != TG_FMT_INTERLEAVED_BLOCKED && kind != TG_FMT_SYMMETRIC)
     e = cudaMemcpyAsync(&totQ, scanQ + Lo.ncell, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return set_cuda_error(e, "tg_build_count");
@@ -432,6 +526,10 @@ int tg_build_count(const int8_t* W, int64_t K, int64_t N, int64_t ldw, int kind,
     sizes->nnz_pos = sizes->nnz_neg = 0;
     sizes->n_indices = totP;
     sizes->offsets_len = Lo.nseg + 1;
+  } else if (kind == TG_FMT_SYMMETRIC) {
+    sizes->nnz_pos = sizes->nnz_neg = 0;
+    sizes->n_indices = totP;
+    sizes->offsets_len = N + 1;
   } else {
     sizes->nnz_pos = totP;
     sizes->nnz_neg = totQ;
@@ -485,6 +583,60 @@ int tg_build_fill_interleaved_blocked(const void* ws, int64_t K, int64_t N, int6
   fill_ib_kernel<<<grid_for(Lo.KW * N), 256, 0, st>>>(P, Q, cpP, cpQ, cellP, cellQ, seg, K, N, B, Lo.KW, g, ai);
   if (symmetric) fill_dummies_kernel<<<grid_for(Lo.ncell), 256, 0, st>>>(cellP, cellQ, seg, Lo.ncell, g, K, ai);
   return check_launch("tg_build_fill_interleaved_blocked");
+}
+
+int tg_build_fill_symmetric(const void* ws, int64_t K, int64_t N, int g, int32_t* indices, int32_t* col_ptr,
+                            int64_t n_indices, void* stream) {
+  if (K < 1 || N < 1 || g < 1 || N % 4 != 0 || !ws || !col_ptr || n_indices < 0)
+    return set_error(TG_ERR_PARAM, "bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Layout Lo = make_layout(K, N, K);
+  const uint32_t* P = at<uint32_t>(ws, Lo.off_P);
+  const uint32_t* Q = at<uint32_t>(ws, Lo.off_Q);
+  const int32_t* cpP = at<int32_t>(ws, Lo.off_cpP);
+  const int32_t* cpQ = at<int32_t>(ws, Lo.off_cpQ);
+  const int64_t* start = at<int64_t>(ws, Lo.off_scanP);
+  ib_offsets_kernel<<<grid_for(N + 1), 256, 0, st>>>(start, N, col_ptr);
+  if (n_indices > 0) {
+    if (!indices) return set_error(TG_ERR_PARAM, "null indices");
+    fill_value_kernel<<<grid_for(n_indices), 256, 0, st>>>(indices, n_indices, int32_t(K));  // dummies
+    fill_sym_kernel<<<grid_for(Lo.KW * N), 256, 0, st>>>(P, Q, cpP, cpQ, start, N, Lo.KW, g, indices);
+  }
+  return check_launch("tg_build_fill_symmetric");
+}
+
+int tg_build_compressed(const int8_t* W, int64_t K, int64_t N, int64_t ldw, uint8_t* codes, void* stream) {
+  if (K < 1 || N < 1) return set_error(TG_ERR_PARAM, "ternary matrix must be 2-D and non-empty");
+  if (ldw < N) return set_error(TG_ERR_PARAM, "ldw must be >= N");
+  if (!W || !codes) return set_error(TG_ERR_PARAM, "null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t G = ceil_div(K, 5);
+  unsigned long long* bad = nullptr;
+  cudaError_t e = cudaMallocAsync(&bad, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaMallocAsync");
+  cudaMemsetAsync(bad, 0xFF, sizeof(unsigned long long), st);
+  compress_kernel<<<grid_for(G * N), 256, 0, st>>>(W, K, N, ldw, G, codes, bad);
+  unsigned long long bad_h = ~0ull;
+  e = cudaMemcpyAsync(&bad_h, bad, sizeof(bad_h), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaFreeAsync(bad, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return set_cuda_error(e, "tg_build_compressed");
+  if (bad_h != ~0ull) {
+    const int64_t k = int64_t(bad_h) / N, n = int64_t(bad_h) % N;
+    int8_t v = 0;
+    cudaMemcpy(&v, W + k * ldw + n, 1, cudaMemcpyDeviceToHost);
+    char msg[160];
+    snprintf(msg, sizeof msg, "entry (%lld, %lld) = %d is not in {-1, 0, +1}", (long long)k, (long long)n, int(v));
+    return set_error(TG_ERR_PARAM, msg);
+  }
+  return TG_OK;
+}
+
+int tg_codes_check(const uint8_t* codes, int64_t count, tg_device_flags* flags, void* stream) {
+  if (count < 0 || (count && (!codes || !flags))) return set_error(TG_ERR_PARAM, "bad arguments");
+  if (count == 0) return TG_OK;
+  codes_check_kernel<<<grid_for(count), 256, 0, static_cast<cudaStream_t>(stream)>>>(codes, count, flags);
+  return check_launch("tg_codes_check");
 }
 
 }  // extern "C"

@@ -125,6 +125,24 @@ int tg_tiles_from_interleaved_blocked(const int32_t* ai, const int32_t* ptr, int
   return run_pack_ib(ai, ptr, N, nb, g, K, tiles, flags, st);
 }
 
+int tg_tiles_from_symmetric(const int32_t* idx, const int32_t* ptr, int64_t K, int64_t N, int g, uint32_t* tiles,
+                            tg_device_flags* flags, void* stream) {
+  TG_REQUIRE(K >= 1 && N >= 1 && g >= 1, TG_ERR_PARAM, "K, N and g must be >= 1");
+  TG_REQUIRE(ptr && tiles, TG_ERR_PARAM, "null pointer");
+  TG_TRY(require_device());
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = cudaMemsetAsync(tiles, 0, tg_tiles_bytes(K, N), st);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaMemsetAsync(tiles)");
+  return run_pack_sym(idx, ptr, N, g, K, tiles, flags, st);
+}
+
+int tg_tiles_from_compressed(const uint8_t* codes, int64_t K, int64_t N, uint32_t* tiles, void* stream) {
+  TG_REQUIRE(K >= 1 && N >= 1, TG_ERR_PARAM, "K and N must be >= 1");
+  TG_REQUIRE(codes && tiles, TG_ERR_PARAM, "null pointer");
+  TG_TRY(require_device());
+  return run_pack_codes(codes, K, N, tiles, as_stream(stream));
+}
+
 int tg_tiles_to_dense(const uint32_t* tiles, int64_t K, int64_t N, int8_t* W, void* stream) {
   TG_REQUIRE(K >= 1 && N >= 1, TG_ERR_PARAM, "K and N must be >= 1");
   TG_REQUIRE(tiles && W, TG_ERR_PARAM, "null pointer");
@@ -160,8 +178,9 @@ int tg_gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, const u
   TG_REQUIRE(M <= (int64_t(1) << 30) && N <= (int64_t(1) << 30), TG_ERR_PARAM, "M, N too large");
   TG_REQUIRE(K <= (int64_t(1) << 24), TG_ERR_PARAM, "K must be < 2^24 for exact int32 limb accumulation");
   if (exact) {
-    TG_REQUIRE(exact->variant >= 0 && exact->variant <= 4, TG_ERR_PARAM, "unknown exact variant");
-    TG_REQUIRE(exact->a0, TG_ERR_PARAM, "exact format without offsets");
+    TG_REQUIRE(exact->variant >= 0 && exact->variant <= 7, TG_ERR_PARAM, "unknown exact variant");
+    TG_REQUIRE(exact->variant == TG_VARIANT_COMPRESSED ? exact->codes != nullptr : exact->a0 != nullptr,
+               TG_ERR_PARAM, "exact format without offsets");
     TG_REQUIRE(exact->B >= 1 && exact->g >= 1 && exact->uf >= 1 && exact->mr >= 1, TG_ERR_PARAM,
                "exact format: B, g, uf, mr must be >= 1");
   }
@@ -175,11 +194,17 @@ int tg_gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, const u
   fx.m_full = (v == TG_VARIANT_BLOCKED) ? M / exact->mr * exact->mr : 0;
   if (v == TG_VARIANT_INTERLEAVED_BLOCKED || v == TG_VARIANT_VECTORIZED_OPTIMAL) {
     fx.var = v == TG_VARIANT_INTERLEAVED_BLOCKED ? VAR_IB : VAR_OPTIMAL;
-    fx.args = GatherArgs{exact->a0, exact->a1, nullptr, nullptr, N, nb, fx.m_full, exact->g, 1};
+    fx.args = GatherArgs{exact->a0, exact->a1, nullptr, nullptr, N, nb, fx.m_full, exact->g, 1, nullptr, 0};
+  } else if (v == TG_VARIANT_VERTICAL || v == TG_VARIANT_HORIZONTAL) {
+    fx.var = v == TG_VARIANT_VERTICAL ? VAR_VERTICAL : VAR_HORIZONTAL;
+    fx.args = GatherArgs{exact->a0, exact->a1, nullptr, nullptr, N, 1, 0, exact->g, 1, nullptr, 0};
+  } else if (v == TG_VARIANT_COMPRESSED) {
+    fx.var = VAR_COMPRESSED;
+    fx.args = GatherArgs{nullptr, nullptr, nullptr, nullptr, N, 1, 0, 1, 1, exact->codes, ceil_div(K, 5)};
   } else {
     fx.var = v == TG_VARIANT_BASE ? VAR_BASE : v == TG_VARIANT_UNROLLED ? VAR_UNROLLED : VAR_BLOCKED;
     fx.args = GatherArgs{exact->a0, exact->a1, exact->a2, exact->a3, N, nb, fx.m_full, 1,
-                         v == TG_VARIANT_BASE ? 1 : exact->uf};
+                         v == TG_VARIANT_BASE ? 1 : exact->uf, nullptr, 0};
   }
   return run_mma(X, M, K, ldx, tiles, N, bias, Y, ldy, use_alpha, alpha, &fx, ws, ws_bytes, flags,
                  as_stream(stream));
@@ -243,6 +268,32 @@ int tg_gemm_interleaved_blocked(const float* X, int64_t M, int64_t K, int64_t ld
   return run_gather(order == TG_ORDER_INTERLEAVED_BLOCKED ? GATHER_IB : GATHER_OPTIMAL, X, M, K, ldx, ptr, ai,
                     nullptr, nullptr, ceil_div(K, B), g, 1, 0, N, bias, Y, ldy, use_alpha, alpha, ws, flags,
                     as_stream(stream));
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int tg_gemm_symmetric(const float* X, int64_t M, int64_t K, int64_t ldx, int g, const int32_t* indices,
+                      const int32_t* col_ptr, int64_t N, const float* bias, float* Y, int64_t ldy, int order,
+                      int use_alpha, float alpha, void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream) {
+  TG_TRY(gather_common_checks(X, M, K, ldx, N, Y, ldy, ws, ws_bytes));
+  TG_REQUIRE(g >= 1, TG_ERR_PARAM, "g must be >= 1");
+  TG_REQUIRE(N % 4 == 0, TG_ERR_PARAM, "N must be divisible by 4");
+  TG_REQUIRE(col_ptr, TG_ERR_PARAM, "null col_ptr");
+  TG_REQUIRE(order == TG_ORDER_VERTICAL || order == TG_ORDER_HORIZONTAL, TG_ERR_PARAM, "unknown order");
+  GatherArgs ga{col_ptr, indices, nullptr, nullptr, N, 1, 0, g, 1, nullptr, 0};
+  return run_gather_args(order == TG_ORDER_VERTICAL ? VAR_VERTICAL : VAR_HORIZONTAL, X, M, K, ldx, ga, bias, Y, ldy,
+                         use_alpha, alpha, ws, flags, as_stream(stream));
+}
+
+int tg_gemm_compressed(const float* X, int64_t M, int64_t K, int64_t ldx, const uint8_t* codes, int64_t N,
+                       const float* bias, float* Y, int64_t ldy, void* ws, size_t ws_bytes, tg_device_flags* flags,
+                       void* stream) {
+  TG_TRY(gather_common_checks(X, M, K, ldx, N, Y, ldy, ws, ws_bytes));
+  TG_REQUIRE(codes, TG_ERR_PARAM, "null codes");
+  GatherArgs ga{nullptr, nullptr, nullptr, nullptr, N, 1, 0, 1, 1, codes, ceil_div(K, 5)};
+  return run_gather_args(VAR_COMPRESSED, X, M, K, ldx, ga, bias, Y, ldy, 0, 0.f, ws, flags, as_stream(stream));
 }
 
 }  // extern "C"

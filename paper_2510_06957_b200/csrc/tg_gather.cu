@@ -110,16 +110,14 @@ int run_transpose(const float* X, int64_t M, int64_t K, int64_t ldx, float* Xt, 
   return check_launch("tg_transpose_kernel");
 }
 
-int run_gather(int variant, const float* X, int64_t M, int64_t K, int64_t ldx, const int32_t* p0, const int32_t* i0,
-               const int32_t* p1, const int32_t* i1, int64_t nblocks, int g, int uf, int64_t m_full, int64_t N,
-               const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, void* ws,
-               tg_device_flags* flags, cudaStream_t st) {
+int run_gather_args(int variant, const float* X, int64_t M, int64_t K, int64_t ldx, const GatherArgs& ga,
+                    const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, void* ws,
+                    tg_device_flags* flags, cudaStream_t st) {
   const int64_t M_pad = round_up(M, G_ROWS);
   float* Xt = static_cast<float*>(ws);
   int rc = run_transpose(X, M, K, ldx, Xt, M_pad, flags, st);
   if (rc != TG_OK) return rc;
-  dim3 grid(unsigned(ceil_div(N, G_WARPS)), unsigned(M_pad / G_ROWS));
-  GatherArgs ga{p0, i0, p1, i1, N, nblocks, m_full, g, uf};
+  dim3 grid(unsigned(ceil_div(ga.N, G_WARPS)), unsigned(M_pad / G_ROWS));
 #define TG_GATHER_LAUNCH(V) \
   tg_gather_kernel<V><<<grid, G_WARPS * 32, 0, st>>>(Xt, M_pad, M, ga, bias, Y, ldy, use_alpha, alpha, flags)
   switch (variant) {
@@ -127,10 +125,21 @@ int run_gather(int variant, const float* X, int64_t M, int64_t K, int64_t ldx, c
     case VAR_UNROLLED: TG_GATHER_LAUNCH(VAR_UNROLLED); break;
     case VAR_BLOCKED: TG_GATHER_LAUNCH(VAR_BLOCKED); break;
     case VAR_IB: TG_GATHER_LAUNCH(VAR_IB); break;
+    case VAR_VERTICAL: TG_GATHER_LAUNCH(VAR_VERTICAL); break;
+    case VAR_HORIZONTAL: TG_GATHER_LAUNCH(VAR_HORIZONTAL); break;
+    case VAR_COMPRESSED: TG_GATHER_LAUNCH(VAR_COMPRESSED); break;
     default: TG_GATHER_LAUNCH(VAR_OPTIMAL); break;
   }
 #undef TG_GATHER_LAUNCH
   return check_launch("tg_gather_kernel");
+}
+
+int run_gather(int variant, const float* X, int64_t M, int64_t K, int64_t ldx, const int32_t* p0, const int32_t* i0,
+               const int32_t* p1, const int32_t* i1, int64_t nblocks, int g, int uf, int64_t m_full, int64_t N,
+               const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, void* ws,
+               tg_device_flags* flags, cudaStream_t st) {
+  GatherArgs ga{p0, i0, p1, i1, N, nblocks, m_full, g, uf, nullptr, 0};
+  return run_gather_args(variant, X, M, K, ldx, ga, bias, Y, ldy, use_alpha, alpha, ws, flags, st);
 }
 
 }  // namespace tg

@@ -964,6 +964,62 @@ __global__ void tg_pack_tiles_ib_kernel(const int32_t* __restrict__ ai, const in
   }
 }
 
+// Symmetric interleaved stream -> tiles.  One warp per column; the sign of
+// stream position t is the run parity (t / g) & 1 (variants.py:622-631).
+__global__ void tg_pack_tiles_sym_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ ptr,
+                                         int64_t N, int g, int64_t K, uint32_t* __restrict__ tiles, int64_t N_pad,
+                                         tg_device_flags* __restrict__ flags) {
+  const int64_t n = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (n >= N) return;
+  const int32_t s = ptr[n], e = ptr[n + 1];
+  for (int32_t i = s + lane; i < e; i += 32) {
+    const int32_t k = idx[i];
+    if (k == K) continue;  // dummy
+    if (k < 0 || k > K) {
+      if (flags) atomicOr(&flags->bad_input, 2);
+      continue;
+    }
+    tile_set(tiles, N_pad, k, n, (((i - s) / g) & 1) != 0, flags);
+  }
+}
+
+// Compressed codes (N x G, 5 base-3 digits per byte, low digit first) -> tiles.
+// One thread per tile word (16 consecutive k of one column).
+__global__ void tg_pack_tiles_codes_kernel(const uint8_t* __restrict__ codes, int64_t K, int64_t N, int64_t G,
+                                           uint32_t* __restrict__ tiles, int64_t KC, int64_t N_pad) {
+  const int64_t total = KC * 8 * N_pad;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t n = idx % N_pad;
+    const int64_t rest = idx / N_pad;
+    const int c = int(rest % 8);
+    const int64_t kc = rest / 8;
+    uint32_t word = 0;
+    if (n < N) {
+      int64_t gi = -1;
+      int code = 121;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int64_t k = kc * 128 + c * 16 + j;
+        if (k < K) {
+          if (k / 5 != gi) {
+            gi = k / 5;
+            code = codes[n * G + gi];
+          }
+          int d = code;
+          for (int t = int(k - 5 * gi); t > 0; --t) d /= 3;
+          d %= 3;  // 0: -1, 1: 0, 2: +1
+          const int bit = 8 * (j & 3) + 2 * (j >> 2);
+          if (d == 2) word |= 1u << bit;
+          else if (d == 0) word |= 3u << bit;
+        }
+      }
+    }
+    tiles[(kc * N_pad + n) * 8 + c] = word;
+  }
+}
+
 // ------------------------------------------------------------------ host launchers
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1322,3 +1378,24 @@ extern "C" int tg_debug_gt(unsigned long long* host_out, int reset) {
   return cudaMemcpyFromSymbol(host_out, tg::g_tg_gt, sizeof(tg::g_tg_gt)) == cudaSuccess ? 0 : 3;
 }
 #endif
+
+namespace tg {
+
+int run_pack_sym(const int32_t* idx, const int32_t* ptr, int64_t N, int g, int64_t K, uint32_t* tiles,
+                 tg_device_flags* flags, cudaStream_t st) {
+  if (N == 0) return TG_OK;
+  tg_pack_tiles_sym_kernel<<<unsigned((N * 32 + 255) / 256), 256, 0, st>>>(idx, ptr, N, g, K, tiles,
+                                                                             round_up(N, 128), flags);
+  return check_launch("tg_pack_tiles_sym_kernel");
+}
+
+int run_pack_codes(const uint8_t* codes, int64_t K, int64_t N, uint32_t* tiles, cudaStream_t st) {
+  const int64_t KC = round_up(K, 128) / 128;
+  const int64_t N_pad = round_up(N, 128);
+  const int64_t total = KC * 8 * N_pad;
+  const unsigned blocks = unsigned(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  tg_pack_tiles_codes_kernel<<<blocks, 256, 0, st>>>(codes, K, N, ceil_div(K, 5), tiles, KC, N_pad);
+  return check_launch("tg_pack_tiles_codes_kernel");
+}
+
+}  // namespace tg

@@ -13,12 +13,26 @@
 //   VAR_IB        kernels/scalar.py:397-485  out=b; per block: acc=0; runs of g (+,-); +rem; -rem; out+=acc
 //   VAR_OPTIMAL   kernels/simd.py:282-420    out=b; per block: acc over the interleaved segment
 //                 (sign = parity of t//g); out+=acc; out+=x (pos rem); out-=x (neg rem)
+//   VAR_VERTICAL  kernels/simd.py:98-188     p, q = run sums of the symmetric stream by run parity
+//                 (t//g)&1; out = (b + p) - q
+//   VAR_HORIZONTAL kernels/simd.py:196-274   a[t%4] +/-= x (sign (t//g)&1); out = b + ((a0+a1)+(a2+a3))
+//   VAR_COMPRESSED kernels/scalar.py:561-602 codes in order, base-3 digits low first (2: +x, 0: -x);
+//                 out = b + acc
 #pragma once
 #include <cstdint>
 
 namespace tg {
 
-enum { VAR_BASE = 0, VAR_BLOCKED = 1, VAR_IB = 2, VAR_OPTIMAL = 3, VAR_UNROLLED = 4 };
+enum {
+  VAR_BASE = 0,
+  VAR_BLOCKED = 1,
+  VAR_IB = 2,
+  VAR_OPTIMAL = 3,
+  VAR_UNROLLED = 4,
+  VAR_VERTICAL = 5,
+  VAR_HORIZONTAL = 6,
+  VAR_COMPRESSED = 7
+};
 
 __device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 __device__ __forceinline__ void add_(float4& a, const float4 b) {
@@ -102,12 +116,14 @@ __device__ __forceinline__ typename S::V banked_sum(const int32_t* __restrict__ 
 }
 
 struct GatherArgs {
-  const int32_t* p0;  // col_start_pos (TCSC / blocked) or col_segment_ptr (interleaved)
-  const int32_t* i0;  // row_index_pos or all_indices
+  const int32_t* p0;  // col_start_pos (TCSC / blocked), col_segment_ptr (interleaved) or col_ptr (symmetric)
+  const int32_t* i0;  // row_index_pos, all_indices or indices (symmetric)
   const int32_t* p1;  // col_start_neg
   const int32_t* i1;  // row_index_neg
   int64_t N, nblocks, m_full;
   int g, uf;
+  const uint8_t* codes;  // compressed: N x G packed base-3 codes
+  int64_t G;
 };
 
 // Y[m, n] before the activation, in the reference's operation order for VAR.
@@ -120,6 +136,48 @@ __device__ __forceinline__ typename S::V column_value(const GatherArgs& a, int64
     V acc = zero_<V>();
     walk<false>(acc, a.i0, __ldg(a.p0 + n), __ldg(a.p0 + n + 1), src);
     walk<true>(acc, a.i1, __ldg(a.p1 + n), __ldg(a.p1 + n + 1), src);
+    return badd_(b, acc);
+  } else if (VAR == VAR_VERTICAL) {
+    const int32_t s = __ldg(a.p0 + n), len = __ldg(a.p0 + n + 1) - s;
+    V p = zero_<V>(), q = zero_<V>();
+    for (int32_t t = 0; t < len; ++t) {
+      const V v = src(__ldg(a.i0 + s + t));
+      if (((t / a.g) & 1) == 0) add_(p, v);
+      else add_(q, v);
+    }
+    V out = badd_(b, p);
+    sub_(out, q);
+    return out;
+  } else if (VAR == VAR_HORIZONTAL) {
+    const int32_t s = __ldg(a.p0 + n), e = __ldg(a.p0 + n + 1);
+    V a0 = zero_<V>(), a1 = zero_<V>(), a2 = zero_<V>(), a3 = zero_<V>();
+    for (int32_t w = s; w < e; w += 4) {
+      const int32_t t = w - s;
+      const V v0 = src(__ldg(a.i0 + w)), v1 = src(__ldg(a.i0 + w + 1));
+      const V v2 = src(__ldg(a.i0 + w + 2)), v3 = src(__ldg(a.i0 + w + 3));
+      if (((t / a.g) & 1) == 0) add_(a0, v0); else sub_(a0, v0);
+      if ((((t + 1) / a.g) & 1) == 0) add_(a1, v1); else sub_(a1, v1);
+      if ((((t + 2) / a.g) & 1) == 0) add_(a2, v2); else sub_(a2, v2);
+      if ((((t + 3) / a.g) & 1) == 0) add_(a3, v3); else sub_(a3, v3);
+    }
+    add_(a0, a1);
+    add_(a2, a3);
+    add_(a0, a2);
+    return badd_(b, a0);
+  } else if (VAR == VAR_COMPRESSED) {
+    V acc = zero_<V>();
+    const uint8_t* c = a.codes + n * a.G;
+    for (int64_t gi = 0; gi < a.G; ++gi) {
+      int code = __ldg(c + gi);
+      if (code == 121) continue;  // five zero digits: no operation (as the reference, which skips zeros)
+#pragma unroll
+      for (int t = 0; t < 5; ++t) {
+        const int d = code % 3;
+        code /= 3;
+        if (d == 2) add_(acc, src(int32_t(5 * gi + t)));
+        else if (d == 0) sub_(acc, src(int32_t(5 * gi + t)));
+      }
+    }
     return badd_(b, acc);
   } else if (VAR == VAR_UNROLLED) {
     const V tot = banked_sum(a.i0, __ldg(a.p0 + n), __ldg(a.p0 + n + 1), a.i1, __ldg(a.p1 + n), __ldg(a.p1 + n + 1),
@@ -179,6 +237,9 @@ __device__ __forceinline__ float column_value_row(int var, const GatherArgs& a, 
     case VAR_UNROLLED: return column_value<VAR_UNROLLED>(a, n, b, src, br);
     case VAR_BLOCKED: return column_value<VAR_BLOCKED>(a, n, b, src, br);
     case VAR_IB: return column_value<VAR_IB>(a, n, b, src, br);
+    case VAR_VERTICAL: return column_value<VAR_VERTICAL>(a, n, b, src, br);
+    case VAR_HORIZONTAL: return column_value<VAR_HORIZONTAL>(a, n, b, src, br);
+    case VAR_COMPRESSED: return column_value<VAR_COMPRESSED>(a, n, b, src, br);
     default: return column_value<VAR_OPTIMAL>(a, n, b, src, br);
   }
 }

@@ -7,6 +7,9 @@ reference builders and fed to either GPU path:
   Tcsc                    tcsc.py:35-68    built by tcsc_from_dense (tcsc.py:71-92)
   BlockedTcsc             variants.py:86-143   blocked_from_dense (variants.py:146-178)
   InterleavedBlockedTcsc  variants.py:251-309  interleaved_blocked_from_dense (variants.py:312-376)
+  SymmetricInterleavedTcsc variants.py:540-580 symmetric_from_dense (variants.py:582-631)
+  CompressedTcsc          variants.py:488-512  compressed_from_dense (variants.py:515-521), with the
+                          5-trits-per-byte codec compress5 / decompress5 / DECODE_TABLE (variants.py:451-485)
 
 Construction runs the two-phase device builder (csrc/tg_build.cu) through the
 C ABI.  Index arrays live on the device; the reference attribute names
@@ -25,7 +28,7 @@ import torch
 
 from . import _native as nat
 from .dense import TernaryDense, _device, _Dual, as_ternary
-from .errors import CorruptionError, ParameterError
+from .errors import CorruptionError, InvalidCodeError, ParameterError
 
 INDEX_DTYPE = np.int32
 DEFAULT_BLOCK_SIZE = 4096
@@ -212,6 +215,139 @@ class InterleavedBlockedTcsc(_Format):
                  _p(self.device("col_segment_ptr")), self.K, self.N, self.B, self.g, _p(t), _p(flags), _stream())
 
 
+class SymmetricInterleavedTcsc(_Format):
+    """One interleaved stream per column, equal lengths inside 4-column groups
+    (variants.py:540-580); column n occupies indices[col_ptr[n]:col_ptr[n+1]]."""
+
+    _arrays = ("indices", "col_ptr")
+
+    def __init__(self, K: int, N: int, g: int, indices, col_ptr):
+        if N % 4 != 0:
+            raise ParameterError(f"N must be divisible by 4, got {N}")
+        if g < 1:
+            raise ParameterError(f"group size must be >= 1, got {g}")
+        self.__dict__.update(K=int(K), N=int(N), g=int(g))
+        ptr = _index_array(col_ptr, "col_ptr")
+        if ptr.shape()[0] != N + 1:
+            raise ParameterError(f"col_ptr must have length N+1 = {N + 1}")
+        self.__dict__["_a"] = {"indices": _index_array(indices, "indices"), "col_ptr": ptr}
+
+    def pairs_in_group(self, group: int) -> int:
+        n = 4 * group
+        p = self.col_ptr
+        return (int(p[n + 1]) - int(p[n])) // 2
+
+    @property
+    def dummy_count(self) -> int:
+        return int((self.device("indices") == self.K).sum().item())
+
+    @property
+    def nnz(self) -> int:
+        return self._len("indices") - self.dummy_count
+
+    def _pack_tiles(self, t, flags):
+        nat.call("tg_tiles_from_symmetric", _p(self.device("indices")), _p(self.device("col_ptr")), self.K, self.N,
+                 self.g, _p(t), _p(flags), _stream())
+
+
+PACK_WIDTH = 5
+CODE_COUNT = 3**PACK_WIDTH
+_POW3 = np.array([3**i for i in range(PACK_WIDTH)], dtype=np.int64)
+
+
+def compress5(values) -> int:
+    """variants.py:451-462: code = sum((v_i + 1) 3^i), little-endian digits."""
+    vals = np.asarray(values, dtype=np.int64)
+    if vals.shape != (PACK_WIDTH,):
+        raise ParameterError(f"compress5 needs exactly {PACK_WIDTH} values, got shape {vals.shape}")
+    if ((vals < -1) | (vals > 1)).any():
+        raise ParameterError(f"values must be in {{-1, 0, +1}}, got {values!r}")
+    return int(((vals + 1) * _POW3).sum())
+
+
+def decompress5(code: int) -> tuple[int, ...]:
+    """variants.py:465-469."""
+    if not 0 <= code < CODE_COUNT:
+        raise InvalidCodeError(f"code must be in [0, {CODE_COUNT}), got {code}")
+    return tuple(int(code // 3**i % 3) - 1 for i in range(PACK_WIDTH))
+
+
+def _decode_table() -> np.ndarray:
+    codes = np.arange(CODE_COUNT, dtype=np.int64)
+    table = ((codes[:, None] // _POW3[None, :]) % 3 - 1).astype(np.int8)
+    table.flags.writeable = False
+    return table
+
+
+DECODE_TABLE = _decode_table()  # variants.py:472-481: DECODE_TABLE[code, i] = i-th ternary digit
+
+
+class CompressedTcsc:
+    """Column-major packed bytes, ceil(K/5) codes per column (variants.py:488-512);
+    codes >= 243 raise InvalidCodeError like the reference constructor."""
+
+    def __init__(self, K: int, N: int, codes):
+        self.K, self.N = int(K), int(N)
+        shape = (self.N, -(-self.K // PACK_WIDTH))
+        if isinstance(codes, torch.Tensor):
+            c = codes.detach().to(torch.uint8).contiguous()
+            if tuple(c.shape) != shape:
+                raise ParameterError(f"codes must have shape {shape}, got {tuple(c.shape)}")
+            if c.is_cuda:
+                flags = torch.zeros(6, dtype=torch.int32, device=c.device)
+                nat.call("tg_codes_check", _p(c), c.numel(), _p(flags), _stream())
+                if int(flags[4].item()) & 4:
+                    bad = int(c[c >= CODE_COUNT][0].item())
+                    raise InvalidCodeError(f"code {bad} is outside [0, {CODE_COUNT})")
+            elif bool((c >= CODE_COUNT).any()):
+                raise InvalidCodeError(f"code {int(c[c >= CODE_COUNT][0])} is outside [0, {CODE_COUNT})")
+            self._c = _Dual(None, c)
+        else:
+            arr = np.ascontiguousarray(codes, dtype=np.uint8)
+            if arr.shape != shape:
+                raise ParameterError(f"codes must have shape {shape}, got {arr.shape}")
+            if (arr >= CODE_COUNT).any():
+                raise InvalidCodeError(f"code {int(arr[arr >= CODE_COUNT][0])} is outside [0, {CODE_COUNT})")
+            self._c = _Dual(arr, None)
+
+    @property
+    def codes(self) -> np.ndarray:
+        return self._c.host()
+
+    def device(self, name: str = "codes") -> torch.Tensor:
+        if name != "codes":
+            raise AttributeError(name)
+        return self._c.dev()
+
+    @property
+    def groups_per_col(self) -> int:
+        return -(-self.K // PACK_WIDTH)
+
+    def format_bytes(self) -> int:
+        """variants.py:495-498: one byte per code (the decode table is program data)."""
+        return self.N * self.groups_per_col
+
+    @property
+    def nnz(self) -> int:
+        return int(np.count_nonzero(DECODE_TABLE[self.codes].reshape(self.N, -1)[:, : self.K]))
+
+    def tiles(self) -> torch.Tensor:
+        t = self.__dict__.get("_tiles")
+        if t is None:
+            nbytes = nat.load().tg_tiles_bytes(self.K, self.N)
+            t = torch.empty(nbytes // 4, dtype=torch.int32, device=_device())
+            nat.call("tg_tiles_from_compressed", _p(self.device()), self.K, self.N, _p(t), _stream())
+            self.__dict__["_tiles"] = t
+        return t
+
+    def to_dense(self) -> TernaryDense:
+        """variants.py:500-503, decoded on the device."""
+        t = self.tiles()
+        w = torch.empty((self.K, self.N), dtype=torch.int8, device=t.device)
+        nat.call("tg_tiles_to_dense", _p(t), self.K, self.N, _p(w), _stream())
+        return TernaryDense(w)
+
+
 # ---------------------------------------------------------------- builders
 
 
@@ -268,6 +404,32 @@ def interleaved_blocked_from_dense(W, B: int | None = None, g: int = DEFAULT_GRO
     nat.call("tg_build_fill_interleaved_blocked", _p(ws), K, N, b, g, int(symmetric_cols), _p(ai), _p(ptr),
              _stream())
     return InterleavedBlockedTcsc(K, N, b, g, ai, ptr, symmetric_cols)
+
+
+def symmetric_from_dense(W, g: int = DEFAULT_GROUP_SIMD) -> SymmetricInterleavedTcsc:
+    """variants.py:582-631, on the device (count -> scan -> fill, dummies = K)."""
+    W = as_ternary(W)
+    if W.N % 4 != 0:
+        raise ParameterError(f"N must be divisible by 4, got {W.N}")
+    if g < 1:
+        raise ParameterError(f"group size must be >= 1, got {g}")
+    ws, s, K, N, dev = _build(W, nat.TG_FMT_SYMMETRIC, W.K, g, False)
+    idx = torch.empty(s.n_indices, dtype=torch.int32, device=dev)
+    ptr = torch.empty(N + 1, dtype=torch.int32, device=dev)
+    nat.call("tg_build_fill_symmetric", _p(ws), K, N, g, _p(idx), _p(ptr), s.n_indices, _stream())
+    return SymmetricInterleavedTcsc(K, N, g, idx, ptr)
+
+
+def compressed_from_dense(W) -> CompressedTcsc:
+    """variants.py:515-521, on the device (validates W like dense.py:45-49)."""
+    W = as_ternary(W)
+    dW = W.device_values
+    K, N = int(dW.shape[0]), int(dW.shape[1])
+    codes = torch.empty((N, -(-K // PACK_WIDTH)), dtype=torch.uint8, device=dW.device)
+    nat.call("tg_build_compressed", _p(dW), K, N, N, _p(codes), _stream())
+    obj = CompressedTcsc.__new__(CompressedTcsc)
+    obj.K, obj.N, obj._c = K, N, _Dual(None, codes)
+    return obj
 
 
 # ---------------------------------------------------------------- utilities

@@ -31,10 +31,14 @@ from .errors import ParameterError
 from .formats import (
     DEFAULT_GROUP_SIMD,
     BlockedTcsc,
+    CompressedTcsc,
     InterleavedBlockedTcsc,
+    SymmetricInterleavedTcsc,
     Tcsc,
     blocked_from_dense,
+    compressed_from_dense,
     interleaved_blocked_from_dense,
+    symmetric_from_dense,
     tcsc_from_dense,
 )
 
@@ -251,6 +255,13 @@ class GemmRunner:
                          "blocked": nat.TG_VARIANT_BLOCKED}[self.kind]
             r.a0, r.a1 = f.device("col_start_pos").data_ptr(), f.device("row_index_pos").data_ptr()
             r.a2, r.a3 = f.device("col_start_neg").data_ptr(), f.device("row_index_neg").data_ptr()
+        elif self.kind in ("vertical", "horizontal"):
+            r.variant = nat.TG_VARIANT_VERTICAL if self.kind == "vertical" else nat.TG_VARIANT_HORIZONTAL
+            r.g = f.g
+            r.a0, r.a1 = f.device("col_ptr").data_ptr(), f.device("indices").data_ptr()
+        elif self.kind == "compressed":
+            r.variant = nat.TG_VARIANT_COMPRESSED
+            r.codes = f.device().data_ptr()
         else:
             r.variant = (nat.TG_VARIANT_VECTORIZED_OPTIMAL if self.kind == "vectorized_optimal"
                          else nat.TG_VARIANT_INTERLEAVED_BLOCKED)
@@ -277,7 +288,13 @@ class GemmRunner:
             return
         if stage == "prepare":
             return
-        if self.kind in ("base", "unrolled"):
+        if self.kind in ("vertical", "horizontal"):
+            order = nat.TG_ORDER_VERTICAL if self.kind == "vertical" else nat.TG_ORDER_HORIZONTAL
+            nat.call("tg_gemm_symmetric", x, M, K, ldx, f.g, _p(f.device("indices")), _p(f.device("col_ptr")), N, b,
+                     y, N, order, self.use_alpha, self.alpha, _p(ws), ws.numel(), fl, st)
+        elif self.kind == "compressed":
+            nat.call("tg_gemm_compressed", x, M, K, ldx, _p(f.device()), N, b, y, N, _p(ws), ws.numel(), fl, st)
+        elif self.kind in ("base", "unrolled"):
             nat.call("tg_gemm_tcsc", x, M, K, ldx, _p(f.device("col_start_pos")), _p(f.device("row_index_pos")),
                      _p(f.device("col_start_neg")), _p(f.device("row_index_neg")), N, b, y, N,
                      0 if self.kind == "base" else self.uf, self.use_alpha, self.alpha, _p(ws), ws.numel(), fl, st)
@@ -425,6 +442,57 @@ def gemm_vectorized_optimal(Xp, t, b, alpha: float | None = None, cfg: GemmConfi
     return _finish(r, counted, Xp.M * (n_idx + t.N * t.num_blocks))
 
 
+def _as_sym(t) -> SymmetricInterleavedTcsc:
+    if isinstance(t, SymmetricInterleavedTcsc):
+        return t
+    return SymmetricInterleavedTcsc(t.K, t.N, t.g, t.indices, t.col_ptr)
+
+
+def _as_compressed(t) -> CompressedTcsc:
+    if isinstance(t, CompressedTcsc):
+        return t
+    return CompressedTcsc(t.K, t.N, t.codes)
+
+
+def _symmetric_kernel(kind: str, Xp, t, b, alpha, counted, method):
+    if not isinstance(Xp, PaddedInput):
+        Xp = PaddedInput(getattr(Xp, "values", Xp))
+    b, t = as_bias(b), _as_sym(t)
+    _check_padded(Xp, t.K, len(b), t.N)
+    _alpha_args(alpha)
+    n_idx = t._len("indices")
+    m = _method(None, method, t.K, t.N, n_idx)
+    r = GemmRunner(kind, Xp.device_values, t, b.device_values, method=m, alpha=alpha)
+    extra = 2 if kind == "vertical" else 4  # simd.py:167-170 (b + p - q) / :253-256 (pairwise + b)
+    return _finish(r, counted, Xp.M * (n_idx + extra * t.N))
+
+
+def gemm_vertical(Xp, t, b, alpha: float | None = None, counted: bool = False, *, method: str | None = None):
+    """kernels/simd.py:98-188 over a SymmetricInterleavedTcsc: run-parity sums p, q; y = (b + p) - q, PReLU.
+    counted: adds = M * (len(indices) + 2N) (dummies included), mults = #(y <= 0) with alpha."""
+    return _symmetric_kernel("vertical", Xp, t, b, alpha, counted, method)
+
+
+def gemm_horizontal(Xp, t, b, alpha: float | None = None, counted: bool = False, *, method: str | None = None):
+    """kernels/simd.py:196-274: four lane sums over the stream, y = b + ((a0 + a1) + (a2 + a3)), PReLU.
+    counted: adds = M * (len(indices) + 4N)."""
+    return _symmetric_kernel("horizontal", Xp, t, b, alpha, counted, method)
+
+
+def gemm_compressed(X, t, b, counted: bool = False, *, method: str | None = None):
+    """kernels/scalar.py:561-602 over 5-trits-per-byte codes: per column, digits in k order
+    (+x for +1, -x for -1), out = b + acc.  counted: adds = M*nnz + M*N, mults = 0."""
+    X, b, t = as_dense(X), as_bias(b), _as_compressed(t)
+    _check_dims(X.cols, t.K, len(b), t.N)
+    m = method if method is not None else "auto"
+    if m == "auto":
+        m = "mma" if t.K <= (1 << 24) else "gather"  # the code stream is dense: density gives no signal
+    m = choose_method(m, t.K, t.N, t.K * t.N)
+    r = GemmRunner("compressed", X.device_values, t, b.device_values, method=m)
+    nnz = t.nnz if counted else 0
+    return _finish(r, counted, X.rows * nnz + X.rows * t.N)
+
+
 # ---------------------------------------------------------------- registry (kernels/__init__.py:66-230)
 
 
@@ -466,6 +534,14 @@ _register(VariantSpec("blocked", "scalar", False, frozenset({"UF", "MR", "NR", "
 _register(VariantSpec("interleaved_blocked", "scalar", False, frozenset({"MR", "NR", "B", "g"}),
                       lambda w, cfg: interleaved_blocked_from_dense(w, cfg.b, _g(cfg, DEFAULT_GROUP_SIMD)), _identity,
                       lambda x, f, b, cfg, counted: gemm_interleaved_blocked(x, f, b, cfg, counted)))
+_register(VariantSpec("compressed", "scalar", False, frozenset(), lambda w, cfg: compressed_from_dense(w), _identity,
+                      lambda x, f, b, cfg, counted: gemm_compressed(x, f, b, counted, method=cfg.method)))
+_register(VariantSpec("vertical", "simd", True, frozenset({"g"}),
+                      lambda w, cfg: symmetric_from_dense(w, _g(cfg, DEFAULT_GROUP_SIMD)), pad_input,
+                      lambda x, f, b, cfg, counted: gemm_vertical(x, f, b, cfg.alpha, counted, method=cfg.method)))
+_register(VariantSpec("horizontal", "simd", True, frozenset({"g"}),
+                      lambda w, cfg: symmetric_from_dense(w, _g(cfg, DEFAULT_GROUP_SIMD)), pad_input,
+                      lambda x, f, b, cfg, counted: gemm_horizontal(x, f, b, cfg.alpha, counted, method=cfg.method)))
 _register(VariantSpec("vectorized_optimal", "simd", True, frozenset({"B", "g"}),
                       lambda w, cfg: interleaved_blocked_from_dense(w, cfg.b, _g(cfg, DEFAULT_GROUP_SIMD),
                                                                     symmetric_cols=True),

@@ -6,11 +6,13 @@ Runs ONLY in the build container, where the reference package is mounted at
 and runs every in-scope reference kernel on seeded integer- and real-valued
 inputs, and writes compact .npz files next to this script:
 
-  formats.npz  W -> Tcsc / BlockedTcsc / InterleavedBlockedTcsc(+symmetric)
-               index arrays, for many shapes, block sizes and group sizes
+  formats.npz  W -> Tcsc / BlockedTcsc / InterleavedBlockedTcsc(+symmetric) /
+               SymmetricInterleavedTcsc / CompressedTcsc arrays, for many
+               shapes, block sizes and group sizes
   kernels.npz  X, b and the reference kernels' fp32 outputs (+ OpCounts) for
                base / unrolled / blocked / interleaved_blocked /
-               vectorized_optimal, plus oracle_gemm, on integer AND real X
+               vectorized_optimal / compressed / vertical / horizontal, plus
+               oracle_gemm, on integer AND real X
   cfg1.npz     the BASELINE cfg1 workload (seed 1, SURVEY.md 8(d) recipe):
                reference Tcsc arrays and gemm_base output
 
@@ -54,7 +56,8 @@ def rand_w(rng, K, N, kind):
 
 
 def put_fmt(store, key, fmt):
-    for name in ("col_start_pos", "row_index_pos", "col_start_neg", "row_index_neg", "all_indices", "col_segment_ptr"):
+    for name in ("col_start_pos", "row_index_pos", "col_start_neg", "row_index_neg", "all_indices", "col_segment_ptr",
+                 "indices", "col_ptr", "codes"):
         if hasattr(fmt, name):
             store[f"{key}.{name}"] = np.asarray(getattr(fmt, name))
 
@@ -103,6 +106,16 @@ def formats_fixture():
                     put_fmt(store, f"{key}.{name2}", f2)
                     entry["formats"].append({"name": name2, "B": B, "g": g, "sym": sym, "resolved_B": f2.B,
                                              "nnz": f2.nnz, "bytes": f2.format_bytes()})
+        # SymmetricInterleavedTcsc (variants.py:540-631) and CompressedTcsc (variants.py:451-532)
+        if N % 4 == 0:
+            for g in (1, 2, 3, 4):
+                f3 = tg.symmetric_from_dense(Wt, g)
+                put_fmt(store, f"{key}.sym_g{g}", f3)
+                entry["formats"].append({"name": f"sym_g{g}", "g": g, "nnz": f3.nnz, "dummies": f3.dummy_count,
+                                         "bytes": f3.format_bytes()})
+        fc = tg.compressed_from_dense(Wt)
+        put_fmt(store, f"{key}.compressed", fc)
+        entry["formats"].append({"name": "compressed", "nnz": fc.nnz, "bytes": fc.format_bytes()})
         index.append(entry)
         cid += 1
     store["index"] = np.frombuffer(json.dumps(index).encode(), dtype=np.uint8)
@@ -160,6 +173,16 @@ def kernels_fixture():
                             rec(f"opt_B{B}_g{g}_a{alpha}",
                                 tg.gemm_vectorized_optimal(Xp, f, bt, alpha, counted=True), B=B, g=g, alpha=alpha,
                                 n_indices=int(f.all_indices.shape[0]), nb=f.num_blocks)
+                rec("compressed", tg.gemm_compressed(Xt, tg.compressed_from_dense(Wt), bt, counted=True))
+                if N % 4 == 0:
+                    Xp = tg.pad_input(Xt)
+                    for g in (2, 1, 3):
+                        f = tg.symmetric_from_dense(Wt, g)
+                        for alpha in (None, 0.25):
+                            rec(f"vertical_g{g}_a{alpha}", tg.gemm_vertical(Xp, f, bt, alpha, counted=True), g=g,
+                                alpha=alpha, n_indices=int(f.indices.shape[0]))
+                            rec(f"horizontal_g{g}_a{alpha}", tg.gemm_horizontal(Xp, f, bt, alpha, counted=True), g=g,
+                                alpha=alpha, n_indices=int(f.indices.shape[0]))
                 for alpha in (None, 0.25):
                     store[f"{key}.oracle_a{alpha}"] = tg.oracle_gemm(Xt, Wt, bt, alpha).values
                 index.append({"key": key, "M": M, "K": K, "N": N, "wkind": kind, "xmode": xmode,

@@ -57,6 +57,20 @@ def test_builders_bit_exact_vs_reference(tg, golden_formats):
             assert np.array_equal(getattr(t, name), arr), (key, "tcsc", name)
         for f in entry["formats"][1:]:
             ref = _fmt_arrays(golden_formats, f"{key}.{f['name']}")
+            if f["name"].startswith("sym_"):
+                got = tg.symmetric_from_dense(W, f["g"])
+                assert got.format_bytes() == f["bytes"] and got.nnz == f["nnz"]
+                assert got.dummy_count == f["dummies"]
+                for name, arr in ref.items():
+                    assert np.array_equal(getattr(got, name), arr), (key, f["name"], name)
+                n += 1
+                continue
+            if f["name"] == "compressed":
+                got = tg.compressed_from_dense(W)
+                assert np.array_equal(got.codes, ref["codes"]), key
+                assert got.format_bytes() == f["bytes"] and got.nnz == f["nnz"]
+                n += 1
+                continue
             if f["name"].startswith("blocked"):
                 got = tg.blocked_from_dense(W, f["B"])
             else:
@@ -107,6 +121,10 @@ def test_round_trips(tg, golden_formats):
         assert np.array_equal(tg.blocked_from_dense(W, 3).to_dense().values, W)
         sym = W.shape[1] % 4 == 0
         assert np.array_equal(tg.interleaved_blocked_from_dense(W, 5, 2, sym).to_dense().values, W)
+        assert np.array_equal(tg.compressed_from_dense(W).to_dense().values, W)
+        if sym:
+            for g_ in (1, 2, 3):
+                assert np.array_equal(tg.symmetric_from_dense(W, g_).to_dense().values, W)
 
 
 def test_builder_rejects_bad_entries(tg):
@@ -152,6 +170,12 @@ def _run_golden(tg, golden, entry, run, method):
         cfg = tg.GemmConfig(mr=run["mr"], b=parse_opt(run["B"]), g=run["g"])
         f = tg.interleaved_blocked_from_dense(W, parse_opt(run["B"]), run["g"])
         return tg.gemm_interleaved_blocked(X, f, b, cfg, counted=True, method=method)
+    if name == "compressed":
+        return tg.gemm_compressed(X, tg.compressed_from_dense(W), b, counted=True, method=method)
+    if name.startswith("vertical") or name.startswith("horizontal"):
+        f = tg.symmetric_from_dense(W, run["g"])
+        fn = tg.gemm_vertical if name.startswith("vertical") else tg.gemm_horizontal
+        return fn(tg.pad_input(X), f, b, run["alpha"], counted=True, method=method)
     f = tg.interleaved_blocked_from_dense(W, parse_opt(run["B"]), run["g"], True)
     return tg.gemm_vectorized_optimal(tg.pad_input(X), f, b, run["alpha"], counted=True, method=method)
 
@@ -195,6 +219,39 @@ def test_worked_example_all_variants_both_paths(tg):
         y = tg.run_variant("vectorized_optimal", X, W4, np.array([10, 20, 0, -1], np.float32),
                            tg.GemmConfig(alpha=0.5, method=method))
         assert y.values.tolist() == [[12.0, 18.0, 0.0, -0.5]]
+
+
+def test_compressed_and_symmetric_full_size(tg):
+    """cfg2's W through the two widened formats: device builders bit-exact with the
+    C oracle, gather kernels bit-exact with the reference order, tensor-core within tolerance."""
+    from paper_2510_06957_b200.workloads import make_inputs
+
+    W, X, b = make_inputs("cfg2", M=64)
+    dW = tg.TernaryDense(torch.from_numpy(W).cuda())
+    c = tg.compressed_from_dense(dW)
+    refc = orc.compressed_from_dense(W)
+    assert np.array_equal(c.codes, refc["codes"])
+    yc = tg.gemm_compressed(X, c, b, method="gather").values
+    assert np.array_equal(yc, orc.gemm_compressed(X, refc, b, threads=8))
+    _assert_tol(tg.gemm_compressed(X, c, b, method="mma").values, X, W, b, None, "compressed mma")
+    s = tg.symmetric_from_dense(dW, 2)
+    refs = orc.symmetric_from_dense(W, 2)
+    assert np.array_equal(s.indices, refs["indices"]) and np.array_equal(s.col_ptr, refs["col_ptr"])
+    Xp = tg.pad_input(X)
+    for name in ("vertical", "horizontal"):
+        fn = getattr(tg, f"gemm_{name}")
+        y = fn(Xp, s, b, 0.25, method="gather").values
+        assert np.array_equal(y, getattr(orc, f"gemm_{name}")(orc.pad_input(X), refs, b, 0.25, threads=8)), name
+        _assert_tol(fn(Xp, s, b, 0.25, method="mma").values, X, W, b, 0.25, name + " mma")
+
+
+def test_invalid_codes_on_device(tg):
+    bad = torch.full((3, 2), 121, dtype=torch.uint8, device="cuda")
+    bad[1, 1] = 250
+    with pytest.raises(tg.InvalidCodeError):
+        tg.CompressedTcsc(10, 3, bad)
+    with pytest.raises(tg.ParameterError):
+        tg.compressed_from_dense(torch.full((5, 2), 2, dtype=torch.int8, device="cuda"))
 
 
 # ---------------------------------------------------------------- BASELINE configs at full size

@@ -30,15 +30,50 @@ def test_config_validation_matches_reference():
 
 
 def test_registry_contract():
-    # kernels/__init__.py:66-80, 200-208: same tags, kinds and alpha support
-    assert tg.SCALAR_TAGS == ("base", "unrolled", "blocked", "interleaved_blocked")
-    assert tg.SIMD_TAGS == ("vectorized_optimal",)
+    # kernels/__init__.py:66-80, 98-208: the reference's tags (in its order), kinds, emit sets and
+    # alpha support; `inverted` (variants.py:384-443) is the one format the paper rejected and is absent
+    assert tg.SCALAR_TAGS == ("base", "unrolled", "blocked", "interleaved_blocked", "compressed")
+    assert tg.SIMD_TAGS == ("vertical", "horizontal", "vectorized_optimal")
     for tag, spec in tg.VARIANTS.items():
         assert spec.tag == tag
-        assert spec.supports_alpha == (tag == "vectorized_optimal")
+        assert spec.supports_alpha == (spec.kind == "simd")
     assert tg.get_variant("blocked").emit == frozenset({"UF", "MR", "NR", "B"})
+    assert tg.get_variant("vertical").emit == frozenset({"g"})
+    assert tg.get_variant("compressed").emit == frozenset()
     with pytest.raises(tg.ParameterError):
         tg.get_variant("inverted")
+
+
+def test_packed_byte_codec():
+    # pkg/tests/test_variants.py:179-212
+    assert tg.compress5([-1] * 5) == 0
+    assert tg.compress5([0] * 5) == 121
+    assert tg.compress5([1] * 5) == 242
+    assert tg.compress5([1, 0, -1, 0, 1]) == 194
+    for code in range(tg.CODE_COUNT):
+        assert tg.compress5(tg.decompress5(code)) == code
+    for code in (tg.CODE_COUNT, 255, -1):
+        with pytest.raises(tg.InvalidCodeError):
+            tg.decompress5(code)
+    with pytest.raises(tg.ParameterError):
+        tg.compress5([0, 0, 0, 2, 0])
+    with pytest.raises(tg.ParameterError):
+        tg.compress5([0, 0, 0])
+    assert tg.DECODE_TABLE.shape == (tg.CODE_COUNT, tg.PACK_WIDTH) and tg.DECODE_TABLE.dtype == np.int8
+    assert not tg.DECODE_TABLE.flags.writeable
+    for code in (0, 121, 194, 242):
+        assert tuple(tg.DECODE_TABLE[code]) == tg.decompress5(code)
+    # host-side construction checks of the compressed and symmetric formats
+    with pytest.raises(tg.InvalidCodeError):
+        tg.CompressedTcsc(4, 1, np.array([[250]], dtype=np.uint8))
+    with pytest.raises(tg.ParameterError):
+        tg.CompressedTcsc(4, 1, np.array([[1, 2]], dtype=np.uint8))
+    c = tg.CompressedTcsc(4, 2, np.array([[140], [118]], dtype=np.uint8))
+    assert c.format_bytes() == 2 and c.groups_per_col == 1 and c.nnz == 4
+    with pytest.raises(tg.ParameterError):
+        tg.SymmetricInterleavedTcsc(4, 3, 2, [], [0, 0, 0, 0])
+    s = tg.SymmetricInterleavedTcsc(8, 4, 2, [0, 1, 2, 3, 8, 8, 8, 8], [0, 8, 8, 8, 8])
+    assert s.format_bytes() == 4 * (8 + 5) and s.pairs_in_group(0) == 4
 
 
 def test_cost_model_pins():
@@ -140,7 +175,7 @@ def test_c_abi_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
     assert set(names) == set(_native.SIGNATURES), set(names) ^ set(_native.SIGNATURES)
     L = _native.load()
-    assert L.tg_abi_version() == 1
+    assert L.tg_abi_version() == 2
     # pure size queries need no device
     assert L.tg_tiles_bytes(4096, 4096) == 32 * 4096 * 8 * 4
     assert L.tg_build_workspace_bytes(4096, 4096, 4096) > 0

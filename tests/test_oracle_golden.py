@@ -67,6 +67,20 @@ def test_formats_match_reference(golden_formats):
             assert np.array_equal(t[name], arr), (key, "tcsc", name)
         for f in entry["formats"][1:]:
             ref = _fmt_keys(golden_formats, f"{key}.{f['name']}")
+            if f["name"].startswith("sym_"):
+                got = orc.symmetric_from_dense(W, f["g"])
+                assert (got["indices"].size + got["col_ptr"].size) * 4 == f["bytes"]
+                assert int((got["indices"] == W.shape[0]).sum()) == f["dummies"]
+                for name, arr in ref.items():
+                    assert np.array_equal(got[name], arr), (key, f["name"], name)
+                checked += 1
+                continue
+            if f["name"] == "compressed":
+                got = orc.compressed_from_dense(W)
+                assert np.array_equal(got["codes"], ref["codes"]), key
+                assert got["codes"].size == f["bytes"]
+                checked += 1
+                continue
             if f["name"].startswith("blocked"):
                 got = orc.blocked_from_dense(W, f["B"])
             else:
@@ -95,6 +109,12 @@ def _check_runs(golden, entry, threads):
         elif name.startswith("ib"):
             y = orc.gemm_interleaved_blocked(X, orc.interleaved_blocked_from_dense(W, run["B"], run["g"]), b,
                                              threads=threads)
+        elif name == "compressed":
+            y = orc.gemm_compressed(X, orc.compressed_from_dense(W), b, threads=threads)
+        elif name.startswith("vertical") or name.startswith("horizontal"):
+            t = orc.symmetric_from_dense(W, run["g"])
+            fn = orc.gemm_vertical if name.startswith("vertical") else orc.gemm_horizontal
+            y = fn(orc.pad_input(X), t, b, run["alpha"], threads=threads)
         else:
             t = orc.interleaved_blocked_from_dense(W, run["B"], run["g"], True)
             y = orc.gemm_vectorized_optimal(orc.pad_input(X), t, b, run["alpha"], threads=threads)
@@ -129,6 +149,23 @@ def test_integer_regime_is_exact_everywhere(golden_kernels):
                 continue
             ref = golden_kernels[f"{key}.oracle_a{alpha}"]
             assert np.array_equal(golden_kernels[f"{key}.{run['name']}"], ref), (key, run["name"])
+
+
+def test_compressed_and_symmetric_known_answers():
+    W, X, b = worked_example()
+    # pkg/tests/test_variants.py:216-224: col0 = [+1, 0, -1, +1] -> 140, col1 = [0, -1, 0, 0] -> 118
+    c = orc.compressed_from_dense(W)
+    assert c["codes"].shape == (2, 1) and c["codes"].tolist() == [[140], [118]]
+    assert orc.gemm_compressed(X, c, b).tolist() == [[12.0, 18.0]]
+    # the SURVEY 8x4 matrix, g = 2: group max(max(p, q)) = 2 -> 4 pairs (lcm(4, 2))
+    W8 = np.zeros((8, 4), np.int8)
+    W8[0:2, 0] = 1
+    W8[2:4, 0] = -1
+    W8[5, 1] = 1
+    s = orc.symmetric_from_dense(W8, 2)
+    assert s["col_ptr"].tolist() == [0, 8, 16, 24, 32]
+    assert s["indices"][:8].tolist() == [0, 1, 2, 3, 8, 8, 8, 8]
+    assert s["indices"][8:16].tolist() == [5, 8, 8, 8, 8, 8, 8, 8]
 
 
 def test_cfg1_pins(golden_cfg1):
