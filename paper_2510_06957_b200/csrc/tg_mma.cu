@@ -35,6 +35,7 @@
 #include <cudaTypedefs.h>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 
 #include "tg_ptx.cuh"
 #include "tg_internal.h"
@@ -383,6 +384,7 @@ struct MmaParams {
   GatherArgs fix;
   const float* X;          // original X (fix-up reads it in place)
   int64_t ldx;
+  int tma_y;               // 1: Y tiles leave through smem + TMA store (ymap), 0: direct stores
 };
 
 // Tile configuration.  A pipeline stage covers 256 k (two 128-k chunks: 8
@@ -405,10 +407,12 @@ struct MmaCfg {
 #ifndef TG_SMEM_BUDGET
 #define TG_SMEM_BUDGET 226000
 #endif
-  // packed-W ring: deep (HBM latency), released by the decoders as soon as they read it
-  static constexpr int P_STAGES = 6;
+  // packed-W ring: released by the decoders as soon as they read it
+  static constexpr int P_STAGES = 4;
+  // Y tile of one unit, written by the epilogue and stored with one TMA bulk-tensor store
+  static constexpr int Y_BYTES = MT * BN * 4;
   // X-limb ring: released by the MMA commit
-  static constexpr int STAGES_RAW = (TG_SMEM_BUDGET - 3072 - P_STAGES * P_BYTES) / B_BYTES;
+  static constexpr int STAGES_RAW = (TG_SMEM_BUDGET - 3072 - P_STAGES * P_BYTES - Y_BYTES) / B_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int ACC_COLS = (NMMA + 31) / 32 * 32;
   static constexpr int A_SLOTS = 2;
@@ -416,12 +420,14 @@ struct MmaCfg {
   static constexpr int ACC_BUFS = (2 * ACC_COLS + A_SLOTS * A_COLS <= 512) ? 2 : 1;
   static constexpr int A_BASE = ACC_BUFS * ACC_COLS;  // first TMEM column of the A ring
   static constexpr int TMEM_COLS = 512;
-  static constexpr int SMEM = STAGES * B_BYTES + P_STAGES * P_BYTES + 1024 /*align*/ + 2048 /*barriers, scales*/;
+  static constexpr int SMEM =
+      STAGES * B_BYTES + P_STAGES * P_BYTES + Y_BYTES + 1024 /*align*/ + 2048 /*barriers, scales*/;
   static constexpr int EPI_WARP0 = 7;            // warps: 0 X producer, 1 MMA, 2-5 decoders, 6 W producer
   static constexpr int EPI_WARPS = 8;            // two per TMEM lane quarter, splitting the rows
   static constexpr int THREADS = 32 * (EPI_WARP0 + EPI_WARPS);
   static_assert(MT % 16 == 0 && NMMA <= 256, "bad MT");
   static_assert(STAGES >= A_SLOTS, "slot release rides on the stage barrier: needs STAGES >= A_SLOTS");
+  static_assert(STAGES >= 3 || MT < 64, "the X ring needs 3 stages at MT = 64");
   static_assert(A_BASE + A_SLOTS * A_COLS <= 512, "TMEM budget");
 };
 
@@ -438,72 +444,135 @@ __device__ __forceinline__ void unit_coords(const MmaParams& p, int u, int crank
   ks1 = int((int64_t(split + 1) * p.KS) / p.splits);
 }
 
-// Finish 16 consecutive rows of one output column: y = fp32(tot * 2^-s + b),
-// PReLU, store.  No FP64 and no 64-bit conversions (each costs ~13 issue cycles
-// per warp on B200, scratch/cvt_bench.cu): tot = H 2^24 + L with 0 <= L < 2^24,
-// so float(H), float(L) are exact and y = fma(H, 2^(24-s), fma(L, 2^-s, b)).
-// The per-row scales {2^-s, 2^(24-s)} are staged as float2 in shared memory;
-// rows whose scale leaves the float range are "wide" and recomputed exactly.
-// Straight-line so the 16 rows pipeline; rows >= M are not stored.
-__device__ __forceinline__ void emit16(const long long (&tot)[16], uint32_t sc_addr, float bf, uint32_t wide_bits,
-                                       const MmaParams& p, int m_first, bool n_ok, float* yrow,
-                                       unsigned long long& npos, bool& bad) {
-  float sc[32];
+// Finish 16 consecutive rows of one output column:
+//   y = fp32(S0 2^(16-s) + S1 2^(8-s) + S2 2^-s + b) with three FMAs on the exact
+//   float limb sums (|S_l| < 2^24), PReLU, and write y into the smem Y tile (or
+//   straight to Y).  No FP64 and no 64-bit conversions on this path (each costs
+//   ~13 issue cycles per warp on B200, scratch/cvt_bench.cu).  For integer-valued
+//   X the low limbs are zero and every step is exact.  The per-row scales
+//   {2^-s, 2^(8-s), 2^(16-s), 2^(24-s)} are staged in shared memory; rows whose
+//   scale leaves the float range are "wide" and recomputed exactly afterwards
+//   (or, without an exact-order format, here in full-range fp64).
+struct EmitCtx {
+  uint32_t sc_addr;  // smem address of the float4 scales of row m_first
+  float bf;
+  uint32_t wide_bits;
+  int m_first;
+  int nlive;   // rows of this chunk inside Y (counting, fp64 fall-back)
+  int nvalid;  // rows to store (16 into the smem tile: the TMA store clips rows >= M)
+  bool n_ok;
+  bool to_smem;      // true: st.shared into the Y tile at ysmem (row stride 512 bytes)
+  uint32_t ysmem;
+  float* ydst;       // false: Y (row stride ldy)
+  int64_t ystride;
+};
+
+__device__ __forceinline__ void load_scales(uint32_t addr, float4 (&sc)[16]) {
 #pragma unroll
-  for (int j = 0; j < 32; j += 4) {
+  for (int j = 0; j < 16; ++j)
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(sc[j]), "=f"(sc[j + 1]), "=f"(sc[j + 2]), "=f"(sc[j + 3])
-                 : "r"(sc_addr + 4u * j));
+                 : "=f"(sc[j].x), "=f"(sc[j].y), "=f"(sc[j].z), "=f"(sc[j].w)
+                 : "r"(addr + 16u * j));
+}
+
+// tail shared by both emitters: PReLU, PReLU count, finiteness, the rare fp64 rows, store
+__device__ __forceinline__ void emit_tail(float (&v)[16], const long long* tot_or_null, const uint32_t* r0,
+                                          const uint32_t* r1, const uint32_t* r2, const EmitCtx& e,
+                                          const MmaParams& p, unsigned long long& npos, bool& bad) {
+  const bool fix = p.fix_var >= 0;
+  if (!fix && e.wide_bits) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (((e.wide_bits >> j) & 1u) && j < e.nlive) {
+        const long long t = tot_or_null ? tot_or_null[j]
+                                        : (static_cast<long long>(static_cast<int>(r0[j])) << 16) +
+                                              (static_cast<long long>(static_cast<int>(r1[j])) << 8) +
+                                              static_cast<long long>(static_cast<int>(r2[j]));
+        v[j] = static_cast<float>(fma(static_cast<double>(t), fabs(__ldg(p.rscale + e.m_first + j)), double(e.bf)));
+      }
+    }
   }
-  const int nvalid = min(16, p.M - m_first);  // rows of this chunk inside Y
-  float y[16];
-  uint32_t negbits = 0;
   float mx = 0.f;
-  const float alpha = p.use_alpha ? p.alpha : 1.f;
+  if (p.use_alpha) {
+    const float alpha = p.alpha;
+    // the reference's `mults`: #(y <= 0) with PReLU; wide rows are counted by the fix-up
+    if (e.nlive >= 16 && !(fix && e.wide_bits)) {
+      unsigned cnt = 0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const bool neg = !(v[j] > 0.f);
+        cnt += neg;
+        v[j] = neg ? alpha * v[j] : v[j];
+        mx = fmaxf(mx, fabsf(v[j]));
+      }
+      if (e.n_ok) npos += cnt;
+    } else {
+      uint32_t negbits = 0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const bool neg = !(v[j] > 0.f);
+        negbits |= uint32_t(neg) << j;
+        v[j] = neg ? alpha * v[j] : v[j];
+        mx = fmaxf(mx, fabsf(v[j]));
+      }
+      const uint32_t live = e.nlive > 0 ? (e.nlive >= 16 ? 0xFFFFu : (1u << e.nlive) - 1u) : 0u;
+      if (e.n_ok) npos += __popc(negbits & live & ~(fix ? e.wide_bits : 0u));
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) mx = fmaxf(mx, fabsf(v[j]));  // padded rows / columns are exactly b or 0
+  }
+  if (!e.n_ok) return;
+  bad |= !(mx <= 3.402823466e38f);
+  if (e.to_smem) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(e.ysmem + 512u * uint32_t(j)), "f"(v[j]) : "memory");
+    return;
+  }
+  if (e.nvalid >= 16) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) e.ydst[int64_t(j) * e.ystride] = v[j];
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < e.nvalid) e.ydst[int64_t(j) * e.ystride] = v[j];
+  }
+}
+
+// from the three limb sums of a finished accumulator (TMEM)
+__device__ __forceinline__ void emit16_limbs(const uint32_t (&r0)[16], const uint32_t (&r1)[16],
+                                             const uint32_t (&r2)[16], const EmitCtx& e, const MmaParams& p,
+                                             unsigned long long& npos, bool& bad) {
+  float4 sc[16];
+  load_scales(e.sc_addr, sc);
+  float v[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    v[j] = __fmaf_rn(float(int(r0[j])), sc[j].z,
+                     __fmaf_rn(float(int(r1[j])), sc[j].y, __fmaf_rn(float(int(r2[j])), sc[j].x, e.bf)));
+  emit_tail(v, nullptr, r0, r1, r2, e, p, npos, bad);
+}
+
+// from reduced int64 sums (split-K): tot = H 2^24 + L, both exact floats
+__device__ __forceinline__ void emit16_tot(const long long (&tot)[16], const EmitCtx& e, const MmaParams& p,
+                                           unsigned long long& npos, bool& bad) {
+  float4 sc[16];
+  load_scales(e.sc_addr, sc);
+  float v[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int lo = int(uint32_t(tot[j]) & 0xFFFFFFu);
     const int hi = int(tot[j] >> 24);
-    const float v = __fmaf_rn(float(hi), sc[2 * j + 1], __fmaf_rn(float(lo), sc[2 * j], bf));
-    const bool neg = !(v > 0.f);
-    negbits |= uint32_t(neg) << j;
-    y[j] = neg ? alpha * v : v;  // alpha = 1 without PReLU: y = v exactly
-    mx = fmaxf(mx, fabsf(y[j]));  // padded rows / columns are exactly b or 0: finite
+    v[j] = __fmaf_rn(float(hi), sc[j].w, __fmaf_rn(float(lo), sc[j].x, e.bf));
   }
-  // Rows whose scale leaves the fp32 range and have no exact-order fix-up: redo in
-  // full-range fp64, behind a branch that the common path never takes, so the
-  // XU-class fp64 conversions are not issued (not even predicated off).
-  const bool fix = p.fix_var >= 0;
-  if (!fix && wide_bits) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      if (((wide_bits >> j) & 1u) && j < nvalid) {
-        float v =
-            static_cast<float>(fma(static_cast<double>(tot[j]), fabs(__ldg(p.rscale + m_first + j)), double(bf)));
-        v = (p.use_alpha && !(v > 0.f)) ? p.alpha * v : v;
-        mx = fmaxf(mx, fabsf(v));
-        y[j] = v;
-      }
-    }
-  }
-  if (!n_ok) return;
-  bad |= !(mx <= 3.402823466e38f);
-  const uint32_t live = nvalid >= 16 ? 0xFFFFu : (nvalid > 0 ? (1u << nvalid) - 1u : 0u);
-  // the reference's `mults`: #(y <= 0) with PReLU; wide rows are counted by the fix-up
-  if (p.use_alpha) npos += __popc(negbits & live & ~(fix ? wide_bits : 0u));
-  if (nvalid >= 16) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) yrow[int64_t(j) * p.ldy] = y[j];
-  } else {
-#pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if (j < nvalid) yrow[int64_t(j) * p.ldy] = y[j];
-  }
+  emit_tail(v, tot, nullptr, nullptr, nullptr, e, p, npos, bad);
 }
 
 template <int MT, int CS>
 __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
-    tg_mma_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ MmaParams p) {
+    tg_mma_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
+                  const __grid_constant__ MmaParams p) {
   using C = MmaCfg<MT>;
   static_assert(CS == 1 || CS == 2 || CS == 4, "cluster size");
   static_assert(MT / CS >= 8, "multicast slices must be whole 8-row swizzle atoms");
@@ -517,7 +586,8 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
   constexpr int SP = C::P_STAGES;
   uint8_t* sB = smem;                       // S x B_BYTES (multiples of 1024)
   uint8_t* sP = sB + S * C::B_BYTES;        // SP x P_BYTES
-  uint64_t* full_raw = reinterpret_cast<uint64_t*>(sP + SP * C::P_BYTES);  // [S] X limbs landed
+  float* ytile = reinterpret_cast<float*>(sP + SP * C::P_BYTES);  // [MT][BN] fp32 (1024-aligned)
+  uint64_t* full_raw = reinterpret_cast<uint64_t*>(sP + SP * C::P_BYTES + C::Y_BYTES);  // [S] X limbs landed
   uint64_t* empty = full_raw + S;           // [S]  MMAs of the stage done (all cluster CTAs)
   uint64_t* p_full = empty + S;             // [SP] packed W landed
   uint64_t* p_empty = p_full + SP;          // [SP] decoders done reading it
@@ -526,7 +596,8 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
   uint64_t* tempty = tfull + 2;             // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int32_t* last_flag = reinterpret_cast<int32_t*>(tmem_slot + 1);
-  // [80] float2 row scales {2^-s, 2^(24-s)} of the current unit (16-byte aligned), then [4] wide-row masks
+  // [80] float4 row scales {2^-s, 2^(8-s), 2^(16-s), 2^(24-s)} of the current unit (16-byte
+  // aligned), then [4] wide-row masks
   double* rs_s = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(tmem_slot + 2) + 15) & ~uintptr_t(15));
 
   const int warp = threadIdx.x >> 5;
@@ -552,6 +623,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
     }
     fence_mbar_init();
     tma_prefetch_desc(&xmap);
+    if (p.tma_y) tma_prefetch_desc(&ymap);
   }
   if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
   tc_fence_before();
@@ -560,9 +632,10 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) TG_STAMP(7, 1);
-  // Programmatic dependent launch: everything above overlapped the X split; its
-  // limbs and row scales are read below this point.
-  grid_dep_wait();
+  // Programmatic dependent launch: everything above overlapped the X split.  Only
+  // the X producer (limbs) and the epilogue (row scales) read its output and wait
+  // for it; the W producer and the decoders start on the packed tiles at once.
+  if (warp == 0 || warp >= C::EPI_WARP0) grid_dep_wait();
   if (threadIdx.x == 0) TG_GT(3);
 
   if (warp == 0) {
@@ -725,14 +798,15 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
     }
   } else {
     // ---------------- epilogue (warps 7..14): warp w owns TMEM lane quarter w%4
-    // (32 output columns) and the 16-row chunks of parity `half`.
+    // (32 output columns) and the 16-row chunks of parity `half`.  The unit's Y
+    // tile is assembled in shared memory and leaves with one TMA store.
     constexpr int ET = 32 * C::EPI_WARPS;
     const int q = warp & 3;
     const int et = threadIdx.x - 32 * C::EPI_WARP0;  // 0..ET-1
     const int half = (warp - C::EPI_WARP0) >> 2;
     const uint32_t rs_addr = smem_u32(rs_s);
-    float2* sc_s = reinterpret_cast<float2*>(rs_s);
-    uint32_t* wmask = reinterpret_cast<uint32_t*>(rs_s + 80);  // [4] wide-row bits of the unit
+    float4* sc_s = reinterpret_cast<float4*>(rs_s);
+    uint32_t* wmask = reinterpret_cast<uint32_t*>(rs_s + 160);  // [4] wide-row bits of the unit (after 80 float4)
     bool any_bad = false;
     unsigned long long npos = 0;
     uint32_t lu = 0;
@@ -742,14 +816,19 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
       const bool ghost = nb >= p.NB;
       const int n0 = nb * C::BN, m0 = mb * MT;
       const uint32_t acc = lu % NACC, use = lu / NACC;
-      const int n = n0 + q * 32 + lane;
+      const int c = q * 32 + lane;  // column inside the tile
+      const int n = n0 + c;
       const bool n_ok = n < p.N;
       const float bf = (n_ok && p.bias) ? __ldg(p.bias + n) : 0.f;
-      // stage the unit's row scales (and which rows are "wide") in shared memory
-      named_bar_sync(1, ET);  // previous unit is done with rs_s / wmask
-      {
+      // previous unit: its TMA store must have read the Y tile, everyone done with the scales
+      if (et == 0 && p.tma_y) bulk_wait_group_read0();
+      named_bar_sync(1, ET);
+      {  // stage the unit's row scales (and which rows are "wide") in shared memory
         const double rs = et < MT ? __ldcg(p.rscale + m0 + et) : 0.0;
-        if (et < MT) sc_s[et] = make_float2(float(fabs(rs)), float(fabs(rs) * 16777216.0));
+        if (et < MT) {
+          const double a = fabs(rs);
+          sc_s[et] = make_float4(float(a), float(a * 256.0), float(a * 65536.0), float(a * 16777216.0));
+        }
         const uint32_t wbits = __ballot_sync(0xffffffffu, rs < 0.0);
         if (lane == 0 && (et >> 5) < 4) wmask[et >> 5] = wbits;
       }
@@ -759,7 +838,22 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
       tc_fence_after();
       const uint32_t tbase = tmem_base + acc * C::ACC_COLS + (uint32_t(q * 32) << 16);
       bool final_writer = p.splits == 1;
-      float* yrow = p.Y + int64_t(m0) * p.ldy + n;
+      auto ctx = [&](int mm) {
+        EmitCtx e;
+        e.sc_addr = rs_addr + 16u * uint32_t(mm);
+        e.bf = bf;
+        e.wide_bits = (wmask[mm >> 5] >> (mm & 31)) & 0xFFFFu;
+        e.m_first = m0 + mm;
+        e.nlive = min(16, p.M - (m0 + mm));
+        e.nvalid = e.nlive;
+        e.n_ok = n_ok;
+        static_assert(C::BN * 4 == 512, "Y tile row pitch");
+        e.to_smem = p.tma_y != 0;  // the TMA store clips rows >= M
+        e.ysmem = smem_u32(ytile) + uint32_t(mm * C::BN + c) * 4u;
+        e.ydst = p.Y + int64_t(m0 + mm) * p.ldy + n;
+        e.ystride = p.ldy;
+        return e;
+      };
 #pragma unroll 1
       for (int mm = 16 * half; mm < MT; mm += 32) {
         if (et == 0 && lu == 0) TG_STAMP(7, 200 + mm / 16);
@@ -773,22 +867,17 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
         tmem_ld16(tbase + 2 * MT + mm, r2);
         tmem_ld_wait();
 #endif
-        if (et == 0 && lu == 0) TG_STAMP(7, 100 + mm / 16);
-        long long tot[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-          tot[j] = (static_cast<long long>(static_cast<int>(r0[j])) << 16) +
-                   (static_cast<long long>(static_cast<int>(r1[j])) << 8) +
-                   static_cast<long long>(static_cast<int>(r2[j]));
         if (et == 0 && lu == 0) TG_STAMP(7, 220 + mm / 16);
         if (p.splits == 1) {
-          emit16(tot, rs_addr + uint32_t(mm) * 8u, bf, (wmask[mm >> 5] >> (mm & 31)) & 0xFFFFu, p, m0 + mm, n_ok,
-                 yrow + int64_t(mm) * p.ldy, npos, any_bad);
+          emit16_limbs(r0, r1, r2, ctx(mm), p, npos, any_bad);
           if (et == 0 && lu == 0) TG_STAMP(7, 240 + mm / 16);
         } else if (!ghost) {
           long long* dst = p.part + (int64_t(split) * p.M_pad + m0 + mm) * p.N_pad + n;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) dst[int64_t(j) * p.N_pad] = tot[j];
+          for (int j = 0; j < 16; ++j)
+            dst[int64_t(j) * p.N_pad] = (static_cast<long long>(static_cast<int>(r0[j])) << 16) +
+                                        (static_cast<long long>(static_cast<int>(r1[j])) << 8) +
+                                        static_cast<long long>(static_cast<int>(r2[j]));
         }
       }
       // TMEM buffer can be reused by the MMA warp
@@ -824,8 +913,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
 #pragma unroll
               for (int j = 0; j < 16; ++j) tot[j] += __ldcg(s2 + int64_t(j) * p.N_pad);
             }
-            emit16(tot, rs_addr + uint32_t(j0) * 8u, bf, (wmask[j0 >> 5] >> (j0 & 31)) & 0xFFFFu, p, m0 + j0, n_ok,
-                   yrow + int64_t(j0) * p.ldy, npos, any_bad);
+            emit16_tot(tot, ctx(j0), p, npos, any_bad);
           }
         }
         named_bar_sync(1, ET);  // last_flag is reused by the next unit
@@ -847,11 +935,21 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
               ++npos;
             }
             any_bad |= !isfinite(y);
-            p.Y[int64_t(m) * p.ldy + n] = y;
+            if (p.tma_y) ytile[j * C::BN + c] = y;
+            else p.Y[int64_t(m) * p.ldy + n] = y;
           }
         }
       }
+      if (p.tma_y && final_writer && !ghost) {
+        fence_proxy_async_smem();  // our st.shared -> visible to the TMA (async proxy)
+        named_bar_sync(1, ET);
+        if (et == 0) {
+          tma_store_2d(&ymap, ytile, n0, m0);
+          bulk_commit_group();
+        }
+      }
     }
+    if (et == 0 && p.tma_y) bulk_wait_group0();
     if (et == 0) TG_STAMP(7, 3 + 2 * (lu - 1));
     if (et == 0) TG_GT(6);
     if (p.flags) {
@@ -1169,10 +1267,10 @@ int run_xsplit(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size
     tg_xsplit_reg_kernel<T, E><<<grid, T, 0, st>>>(X, M, K, ldx, limbs, rscale, L.M_pad, L.K_pad, flags);  \
     return check_launch("tg_xsplit_reg_kernel");                                                               \
   }
-  if (L.M_pad <= 4 * num_sms()) {  // few rows: wide CTAs so the whole GPU has loads in flight
-    TG_XS_REG(1024, 4)
-    TG_XS_REG(1024, 8)
-    TG_XS_REG(1024, 16)
+  if (L.M_pad <= 4 * num_sms()) {  // few rows: wide CTAs (two per SM) so the whole GPU has loads in flight
+    TG_XS_REG(512, 4)
+    TG_XS_REG(512, 8)
+    TG_XS_REG(512, 16)
   } else {
     TG_XS_REG(256, 16)
     TG_XS_REG(256, 32)
@@ -1207,7 +1305,8 @@ int run_xsplit(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size
 }
 
 template <int MT, int CS>
-static int launch_mma(const CUtensorMap& map, const MmaParams& p, int grid, cudaStream_t st) {
+static int launch_mma(const CUtensorMap& map, const CUtensorMap& ymap, const MmaParams& p, int grid,
+                      cudaStream_t st) {
   using C = MmaCfg<MT>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -1230,7 +1329,7 @@ static int launch_mma(const CUtensorMap& map, const MmaParams& p, int grid, cuda
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = CS > 1 ? 2 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tg_mma_kernel<MT, CS>, map, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tg_mma_kernel<MT, CS>, map, ymap, p);
   if (e != cudaSuccess) return set_cuda_error(e, "cudaLaunchKernelEx(tg_mma_kernel)");
   return check_launch("tg_mma_kernel");
 }
@@ -1255,7 +1354,22 @@ int run_mma(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* t
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(TG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
 
+  // Y leaves through a TMA store when its layout allows it (16-byte aligned base and row pitch)
+  CUtensorMap ymap;
+  memset(&ymap, 0, sizeof(ymap));
+  int tma_y = 0;
+  if ((reinterpret_cast<uintptr_t>(Y) & 15) == 0 && (ldy * 4) % 16 == 0 && !getenv("TG_MMA_DIRECT_Y")) {
+    cuuint64_t ydim[2] = {cuuint64_t(N), cuuint64_t(M)};
+    cuuint64_t ystride[1] = {cuuint64_t(ldy) * 4};
+    cuuint32_t ybox[2] = {128u, cuuint32_t(L.mt)};
+    cuuint32_t yes[2] = {1u, 1u};
+    if (enc(&ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Y, ydim, ystride, ybox, yes, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      tma_y = 1;
+  }
   MmaParams p{};
+  p.tma_y = tma_y;
   p.tiles = tiles;
   p.rscale = reinterpret_cast<const double*>(base + L.off_rscale);
   p.bias = bias;
@@ -1291,16 +1405,16 @@ int run_mma(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* t
   }
   const int grid = int(std::min<int64_t>(p.units, L.clusters)) * L.cs;
   switch (L.mt * 10 + L.cs) {
-    case 161: return launch_mma<16, 1>(map, p, grid, st);
-    case 162: return launch_mma<16, 2>(map, p, grid, st);
-    case 321: return launch_mma<32, 1>(map, p, grid, st);
-    case 322: return launch_mma<32, 2>(map, p, grid, st);
-    case 324: return launch_mma<32, 4>(map, p, grid, st);
-    case 481: return launch_mma<48, 1>(map, p, grid, st);
-    case 482: return launch_mma<48, 2>(map, p, grid, st);
-    case 641: return launch_mma<64, 1>(map, p, grid, st);
-    case 642: return launch_mma<64, 2>(map, p, grid, st);
-    default: return launch_mma<64, 4>(map, p, grid, st);
+    case 161: return launch_mma<16, 1>(map, ymap, p, grid, st);
+    case 162: return launch_mma<16, 2>(map, ymap, p, grid, st);
+    case 321: return launch_mma<32, 1>(map, ymap, p, grid, st);
+    case 322: return launch_mma<32, 2>(map, ymap, p, grid, st);
+    case 324: return launch_mma<32, 4>(map, ymap, p, grid, st);
+    case 481: return launch_mma<48, 1>(map, ymap, p, grid, st);
+    case 482: return launch_mma<48, 2>(map, ymap, p, grid, st);
+    case 641: return launch_mma<64, 1>(map, ymap, p, grid, st);
+    case 642: return launch_mma<64, 2>(map, ymap, p, grid, st);
+    default: return launch_mma<64, 4>(map, ymap, p, grid, st);
   }
 }
 

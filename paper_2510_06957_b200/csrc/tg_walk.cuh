@@ -53,6 +53,30 @@ template <> __device__ __forceinline__ float4 splat_<float4>(float b) { return m
 __device__ __forceinline__ float badd_(float b, float a) { return b + a; }
 __device__ __forceinline__ float4 badd_(float b, float4 a) { return make_float4(b + a.x, b + a.y, b + a.z, b + a.w); }
 
+// Eight rows of one column (the shared-memory slab kernel's register tile).
+struct F8 {
+  float4 a, b;
+};
+__device__ __forceinline__ void add_(F8& x, const F8 y) { add_(x.a, y.a); add_(x.b, y.b); }
+__device__ __forceinline__ void sub_(F8& x, const F8 y) { sub_(x.a, y.a); sub_(x.b, y.b); }
+template <> __device__ __forceinline__ F8 zero_<F8>() { return F8{zero_<float4>(), zero_<float4>()}; }
+template <> __device__ __forceinline__ F8 splat_<F8>(float b) { return F8{splat_<float4>(b), splat_<float4>(b)}; }
+__device__ __forceinline__ F8 badd_(float b, F8 a) { return F8{badd_(b, a.a), badd_(b, a.b)}; }
+
+// out += (row r banked ? tot : acc), per component (blocked kernel, scalar.py:350-358)
+__device__ __forceinline__ void add_sel_(float& o, float t, float a, unsigned bk) { o += (bk & 1u) ? t : a; }
+__device__ __forceinline__ void add_sel_(float4& o, const float4 t, const float4 a, unsigned bk) {
+  o.x += (bk & 1u) ? t.x : a.x;
+  o.y += (bk & 2u) ? t.y : a.y;
+  o.z += (bk & 4u) ? t.z : a.z;
+  o.w += (bk & 8u) ? t.w : a.w;
+}
+__device__ __forceinline__ void add_sel_(F8& o, const F8 t, const F8 a, unsigned bk) {
+  add_sel_(o.a, t.a, a.a, bk);
+  add_sel_(o.b, t.b, a.b, bk >> 4);
+}
+template <typename V> __device__ __forceinline__ constexpr unsigned lanes_all_() { return (1u << (sizeof(V) / 4)) - 1u; }
+
 // Operand sources: the value X[., k] for a stream index k.
 struct SrcXt {  // 4 consecutive rows from the transposed copy Xt[K+1][M_pad]
   using V = float4;
@@ -65,16 +89,20 @@ struct SrcRow {  // one row of X in place (ldx = K or K+1)
   const float* x;
   __device__ __forceinline__ float operator()(int32_t k) const { return __ldg(x + k); }
 };
-
 // Walk [a, b) of an index stream adding (NEG=false) or subtracting into acc,
 // strictly in stream order.
 template <bool NEG, typename S>
 __device__ __forceinline__ void walk(typename S::V& acc, const int32_t* __restrict__ idx, int32_t a, int32_t b,
                                      const S& src) {
   int32_t i = a;
+  // head up to a 16-byte boundary, then 128-bit index loads
+  for (; i < b && (reinterpret_cast<uintptr_t>(idx + i) & 15u); ++i) {
+    const typename S::V v = src(__ldg(idx + i));
+    if (NEG) sub_(acc, v); else add_(acc, v);
+  }
   for (; i + 4 <= b; i += 4) {
-    const int32_t k0 = __ldg(idx + i), k1 = __ldg(idx + i + 1), k2 = __ldg(idx + i + 2), k3 = __ldg(idx + i + 3);
-    const typename S::V v0 = src(k0), v1 = src(k1), v2 = src(k2), v3 = src(k3);
+    const int4 k = __ldg(reinterpret_cast<const int4*>(idx + i));
+    const typename S::V v0 = src(k.x), v1 = src(k.y), v2 = src(k.z), v3 = src(k.w);
     if (NEG) { sub_(acc, v0); sub_(acc, v1); sub_(acc, v2); sub_(acc, v3); }
     else { add_(acc, v0); add_(acc, v1); add_(acc, v2); add_(acc, v3); }
   }
@@ -191,18 +219,11 @@ __device__ __forceinline__ typename S::V column_value(const GatherArgs& a, int64
       const int32_t ap = __ldg(cp + n), bp = __ldg(cp + n + 1), an = __ldg(cn + n), bn = __ldg(cn + n + 1);
       V tot = zero_<V>(), acc = zero_<V>();
       if (banked_rows) tot = banked_sum(a.i0, ap, bp, a.i1, an, bn, a.uf, src);
-      if (banked_rows != (sizeof(V) == 4 ? 1u : 15u)) {
+      if (banked_rows != lanes_all_<V>()) {
         walk<false>(acc, a.i0, ap, bp, src);
         walk<true>(acc, a.i1, an, bn, src);
       }
-      if constexpr (sizeof(V) == 4) {
-        out += (banked_rows & 1u) ? tot : acc;
-      } else {
-        out.x += (banked_rows & 1u) ? tot.x : acc.x;
-        out.y += (banked_rows & 2u) ? tot.y : acc.y;
-        out.z += (banked_rows & 4u) ? tot.z : acc.z;
-        out.w += (banked_rows & 8u) ? tot.w : acc.w;
-      }
+      add_sel_(out, tot, acc, banked_rows);
     }
     return out;
   } else {
