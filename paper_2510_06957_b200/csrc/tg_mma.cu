@@ -408,7 +408,8 @@ struct MmaCfg {
 #define TG_SMEM_BUDGET 226000
 #endif
   // packed-W ring: released by the decoders as soon as they read it
-  static constexpr int P_STAGES = 4;
+  // (deep for small MT: a decode-like GEMM streams W from HBM and needs many bytes in flight)
+  static constexpr int P_STAGES = MT <= 16 ? 12 : MT <= 32 ? 8 : 4;
   // Y tile of one unit, written by the epilogue and stored with one TMA bulk-tensor store
   static constexpr int Y_BYTES = MT * BN * 4;
   // X-limb ring: released by the MMA commit

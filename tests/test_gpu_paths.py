@@ -1,0 +1,120 @@
+"""Tensor-core path: every code path of the persistent tcgen05 kernel against
+an fp64 reference on the device.
+
+The shapes pick each branch on purpose:
+* MT = 16 / 32 / 48 / 64 (M <= 16, <= 32, <= 48, larger), padded rows;
+* an odd number of 128-k chunks (a half-filled last 256-k stage), K = 1;
+* cluster sizes 1 / 2 / 4 with ghost column blocks (NB not a multiple of CS);
+* split-K with the last-arriving reduction (few tiles, long K);
+* N not a multiple of 4 (direct Y stores instead of the TMA store);
+* the three X-split kernels (register-resident, smem-staged K > 16384,
+  global multi-pass K > 32768).
+
+Integer-valued X must be bit-exact (exact limbs, exact integer accumulation);
+real X within the 1e-5 normwise / |terms|-scaled bars.
+"""
+
+from __future__ import annotations
+
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def tg():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2510_06957_b200 as m
+
+    return m
+
+
+def _ref(X, W, b, alpha=None):
+    y = X.double() @ W.double() + b.double()
+    if alpha is not None:
+        y = torch.where(y > 0, y, alpha * y)
+    return y
+
+
+CASES = [
+    # (M, K, N)
+    (1, 1, 4),
+    (10, 100, 130),       # MT 16, one chunk, N % 4 != 0 -> direct stores
+    (30, 384, 520),       # MT 32, 3 chunks (odd), NB = 5 -> ghost blocks with CS = 4
+    (40, 257, 256),       # MT 48
+    (100, 1000, 384),     # MT 64, padded rows, NB = 3
+    (64, 8192, 128),      # one tile, long K -> split-K
+    (16, 4096, 1024),     # decode-like, split-K
+    (300, 640, 1000),     # NB = 8, N % 128 != 0
+    (24, 20000, 64),      # K > 16384: split staged without shared memory
+    (8, 40000, 32),       # K > 32768: multi-pass split
+]
+
+
+@pytest.mark.parametrize("M,K,N", CASES)
+def test_tensor_core_paths(tg, M, K, N):
+    g = torch.Generator(device="cuda").manual_seed(M * 7919 + K * 31 + N)
+    W = torch.randint(-1, 2, (K, N), device="cuda", generator=g, dtype=torch.int8)
+    Xi = torch.randint(-8, 9, (M, K), device="cuda", generator=g).float()
+    bi = torch.randint(-8, 9, (N,), device="cuda", generator=g).float()
+    t = tg.tcsc_from_dense(tg.TernaryDense(W))
+    y = tg.gemm_base(Xi, t, bi, method="mma").device_values
+    assert torch.equal(y.double(), _ref(Xi, W, bi)), (M, K, N)
+    Xr = torch.randn((M, K), device="cuda", generator=g)
+    br = torch.randn((N,), device="cuda", generator=g)
+    y = tg.gemm_base(Xr, t, br, method="mma").device_values.double()
+    ref = _ref(Xr, W, br)
+    nw = float((y - ref).abs().max() / ref.abs().max().clamp_min(1e-30))
+    scale = Xr.abs().double() @ W.abs().double() + br.abs().double()
+    sc = float(((y - ref).abs() / scale.clamp_min(1e-30)).max())
+    assert nw <= TOL and sc <= TOL, (M, K, N, nw, sc)
+
+
+def test_cluster_sizes_agree(tg, monkeypatch):
+    """The X-limb multicast (cluster of 1, 2 or 4 CTAs) must not change a single bit."""
+    from paper_2510_06957_b200.workloads import make_inputs
+
+    W, X, b = make_inputs("cfg2", M=90)
+    W, b = np.ascontiguousarray(W[:, :1164]), b[:1164]  # NB = 10: ghost blocks for CS = 4
+    t = tg.interleaved_blocked_from_dense(torch.from_numpy(W).cuda(), None, 2, True)
+    Xp = tg.pad_input(torch.from_numpy(X).cuda())
+    ys = []
+    for cs in ("1", "2", "4"):
+        monkeypatch.setenv("TG_MMA_CLUSTER", cs)  # read whenever a launch is planned
+        ys.append(tg.gemm_vectorized_optimal(Xp, t, b, 0.25, method="mma").device_values.clone())
+    assert torch.equal(ys[0], ys[1]) and torch.equal(ys[0], ys[2])
+
+
+def test_wide_rows_without_exact_format_use_fp64(tg):
+    """tg_gemm_tiles with exact == NULL: rows outside the fp32 scale range take the
+    fp64 epilogue branch (no exact-order fix-up available) and stay accurate."""
+    import ctypes
+
+    from paper_2510_06957_b200 import _native as nat
+
+    M, K, N = 20, 300, 64
+    g = torch.Generator(device="cuda").manual_seed(5)
+    W = torch.randint(-1, 2, (K, N), device="cuda", generator=g, dtype=torch.int8)
+    X = torch.randn((M, K), device="cuda", generator=g)
+    X[3] *= 1e-35   # 2^-s far below the float range
+    X[7] *= 1e35    # and far above
+    b = torch.zeros(N, device="cuda")
+    t = tg.tcsc_from_dense(tg.TernaryDense(W))
+    tiles = t.tiles()
+    y = torch.empty((M, N), device="cuda")
+    L = nat.load()
+    ws = torch.empty(L.tg_gemm_workspace_bytes(M, K, N), dtype=torch.uint8, device="cuda")
+    nat.call("tg_gemm_tiles", ctypes.c_void_p(X.data_ptr()), M, K, K, ctypes.c_void_p(tiles.data_ptr()), N,
+             ctypes.c_void_p(b.data_ptr()), ctypes.c_void_p(y.data_ptr()), N, 0, 0.0, None,
+             ctypes.c_void_p(ws.data_ptr()), ws.numel(), None, torch.cuda.current_stream().cuda_stream)
+    ref = _ref(X, W, b)
+    for m in range(M):
+        den = ref[m].abs().max()
+        err = float((y[m].double() - ref[m]).abs().max() / den) if den > 0 else float(y[m].abs().max())
+        assert err <= TOL, (m, err)
