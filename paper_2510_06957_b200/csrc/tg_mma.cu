@@ -411,7 +411,8 @@ struct MmaCfg {
   // (deep for small MT: a decode-like GEMM streams W from HBM and needs many bytes in flight)
   static constexpr int P_STAGES = MT <= 16 ? 12 : MT <= 32 ? 8 : 4;
   // Y tile of one unit, written by the epilogue and stored with one TMA bulk-tensor store
-  static constexpr int Y_BYTES = MT * BN * 4;
+  // (none at MT = 80: the X ring needs the room; that tile size stores Y directly)
+  static constexpr int Y_BYTES = MT >= 80 ? 0 : MT * BN * 4;
   // X-limb ring: released by the MMA commit
   static constexpr int STAGES_RAW = (TG_SMEM_BUDGET - 3072 - P_STAGES * P_BYTES - Y_BYTES) / B_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
@@ -1143,10 +1144,19 @@ static int num_sms() {
 }
 
 int mma_pick_mt(int64_t M) {
+  if (const char* env = getenv("TG_MMA_MT")) {
+    const int v = atoi(env);
+    if (v == 16 || v == 32 || v == 48 || v == 64 || v == 80) return v;
+  }
   if (M <= 16) return 16;
   if (M <= 32) return 32;
   if (M <= 48) return 48;
-  return 64;  // N = 192: two TMEM accumulators + a 4-slot A ring fit the 512 columns
+  // MT = 80 (MMA N = 240) hides the per-stage commit inside the longer MMAs (scratch/mma_bench.cu:
+  // 131 cycles per 128x240x32 MMA with a commit every 8, at the issue-rate peak) but has room for
+  // one TMEM accumulator only, so its epilogue is not overlapped: worth it for tall X (many units
+  // per CTA) whose padding to 80 rows is small.
+  if (M >= 2048 && round_up(M, 80) * 100 <= round_up(M, 64) * 102) return 80;
+  return 64;  // N = 192: two TMEM accumulators + a 2-slot A ring fill the 512 columns
 }
 
 // K splits per (column group, row block) tile: minimise rounds x (stages + overhead)
@@ -1219,6 +1229,8 @@ static int max_clusters_for(int64_t mt, int cs) {
     case 482: return max_clusters<48, 2>();
     case 641: return max_clusters<64, 1>();
     case 642: return max_clusters<64, 2>();
+    case 801: return max_clusters<80, 1>();
+    case 802: return max_clusters<80, 2>();
     default: return max_clusters<64, 4>();
   }
 }
@@ -1316,6 +1328,8 @@ static int launch_mma(const CUtensorMap& map, const CUtensorMap& ymap, const Mma
     if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(tg_mma_kernel)");
     attr_set = true;
   }
+  MmaParams pp = p;
+  if (C::Y_BYTES == 0) pp.tma_y = 0;  // no smem Y tile at this tile size
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(grid));
   cfg.blockDim = dim3(C::THREADS);
@@ -1330,7 +1344,7 @@ static int launch_mma(const CUtensorMap& map, const CUtensorMap& ymap, const Mma
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = CS > 1 ? 2 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tg_mma_kernel<MT, CS>, map, ymap, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tg_mma_kernel<MT, CS>, map, ymap, pp);
   if (e != cudaSuccess) return set_cuda_error(e, "cudaLaunchKernelEx(tg_mma_kernel)");
   return check_launch("tg_mma_kernel");
 }
@@ -1415,6 +1429,8 @@ int run_mma(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* t
     case 482: return launch_mma<48, 2>(map, ymap, p, grid, st);
     case 641: return launch_mma<64, 1>(map, ymap, p, grid, st);
     case 642: return launch_mma<64, 2>(map, ymap, p, grid, st);
+    case 801: return launch_mma<80, 1>(map, ymap, p, grid, st);
+    case 802: return launch_mma<80, 2>(map, ymap, p, grid, st);
     default: return launch_mma<64, 4>(map, ymap, p, grid, st);
   }
 }
