@@ -342,11 +342,13 @@ def run_ours(args) -> None:
 
     # ---- breakdown (same loop-difference method, direct launches):
     #   prepare = K x (flush + X split) - K x flush;  run = K x (flush + split + GEMM) - K x (flush + split)
+    n_bd = max(args.steps, 20)  # enough repetitions for the differences to be above timer noise
+
     def loop_ms(fn):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(n_bd):
             flush.zero_()
             fn()
         e1.record(stream)
@@ -356,13 +358,13 @@ def run_ours(args) -> None:
     t_f = loop_ms(lambda: None)
     t_fp = loop_ms(lambda: runner.launch(stage="prepare"))
     t_fpr = loop_ms(lambda: (runner.launch(stage="prepare"), runner.launch(stage="run")))
-    t_prep = max(t_fp - t_f, 0.0) / args.steps
-    t_run = max(t_fpr - t_fp, 0.0) / args.steps
+    t_prep = max(t_fp - t_f, 0.0) / n_bd
+    t_run = max(t_fpr - t_fp, 1e-6) / n_bd
     t_comm = 0.0
     if world > 1:
         t_fpra = loop_ms(lambda: (runner.launch(stage="prepare"), runner.launch(stage="run"),
                                   part.assemble(runner.y, y_full)))
-        t_comm = max(t_fpra - t_fpr, 0.0) / args.steps
+        t_comm = max(t_fpra - t_fpr, 0.0) / n_bd
     t_step_max = max_over_ranks(t_step, world, dev)
 
     total_ops = ops(M, N, nnz_total)
@@ -417,7 +419,7 @@ def run_ours(args) -> None:
     w_loc = sh.width
     ops_loc = ops(M, w_loc, nnz_local)
     bytes_loc = algorithmic_bytes(M, K, w_loc, nnz_local)
-    t_kernel = t_run if method == "mma" else t_prep + t_run
+    t_kernel = max(t_run if method == "mma" else t_prep + t_run, 1e-6)
     kern_name = "tg_mma_kernel" if method == "mma" else "tg_gather_kernel"
     t_add = ops_loc / (p_add * 1e12)
     t_hbm = bytes_loc / (NOMINAL_HBM_GBS * 1e9)
