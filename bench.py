@@ -288,9 +288,59 @@ def run_ours(args) -> None:
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
     stream = torch.cuda.current_stream()
 
-    graph = None if args.no_graph else runner.capture()
+    # ---- shard assembly (N > 1): the fused peer-store epilogue by default, NCCL on request
+    assembly = "none" if world == 1 else args.assembly
+    asm_note = None
+    if assembly == "peer" and method != "mma":
+        assembly, asm_note = "nccl", "gather method has no fused epilogue; NCCL all-gather"
+    sg = bufs = None
+    if assembly == "peer":
+        from paper_2510_06957_b200.peer import PeerYBuffers, ScatterGemm
+
+        bufs = PeerYBuffers(M, N, symmetric=sym)
+        assert bufs.shard == sh, (bufs.shard, sh)
+        sg = ScatterGemm(lambda out, scatter: GemmRunner(kind, xin, fmt, db, method=method, alpha=wl.alpha, out=out,
+                                                         scatter=scatter), bufs)
+        for r in sg.runners:
+            r.pin_workspace()
+        # validate once: the kernel-assembled Y equals the NCCL-assembled Y bit for bit, on every slot
+        y_nccl = part.assemble(runner.y, y_full).clone()
+        ok = True
+        for _ in range(2 * bufs.slots):
+            yf = sg.step()
+            torch.cuda.synchronize()
+            ok = ok and bool(torch.equal(yf, y_nccl)) and not bufs.timed_out()
+        if max_over_ranks(0.0 if ok else 1.0, world, dev) != 0.0:
+            assembly, asm_note = "nccl", "peer scatter failed validation on some rank; fell back to NCCL all-gather"
+            sg = None
+        del y_nccl
+
+    def capture(fn):
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                fn()
+        torch.cuda.current_stream().wait_stream(s)
+        return g
+
+    graphs = None
+    if not args.no_graph:
+        if sg is not None:  # one graph per Y slot: shard GEMM with the peer scatter + arrival wait
+            graphs = [capture(lambda r=r: (r.launch(), bufs.wait())) for r in sg.runners]
+        else:
+            graphs = [runner.capture()]
+    graph = graphs[0] if graphs else None
 
     def step():
+        if sg is not None:  # slots strictly alternate (ScatterGemm's counter), graph or not
+            if graphs is not None:
+                graphs[sg.slot].replay()
+                sg.n += 1
+            else:
+                sg.step()
+            return
         if graph is not None:
             graph.replay()
         else:
@@ -329,12 +379,17 @@ def run_ours(args) -> None:
         flush.zero_()
     e_all[3].record(stream)
     torch.cuda.synchronize()
-    # keep the GPU loaded until the clock sampler has ~1 s of samples (untimed)
-    while time.perf_counter() - t_clk0 < 1.2:
-        for _ in range(20):
-            flush.zero_()
-            step()
-        torch.cuda.synchronize()
+    # keep the GPU loaded until the clock sampler has ~1 s of samples (untimed); the
+    # iteration count is agreed over ranks (every rank must run the same steps)
+    per_it = max(e_all[0].elapsed_time(e_all[1]) / max(args.steps, 1), 1e-3) * 1e-3
+    n_more = int(max(0.0, 1.2 - (time.perf_counter() - t_clk0)) / per_it) + 1
+    n_more = int(max_over_ranks(float(min(n_more, 200000)), world, dev))
+    for i in range(n_more):
+        flush.zero_()
+        step()
+        if i % 64 == 63:
+            torch.cuda.synchronize()
+    torch.cuda.synchronize()
     clk = clocks.stop()
     t_with = e_all[0].elapsed_time(e_all[1])
     t_flush = e_all[2].elapsed_time(e_all[3])
@@ -361,7 +416,10 @@ def run_ours(args) -> None:
     t_prep = max(t_fp - t_f, 0.0) / n_bd
     t_run = max(t_fpr - t_fp, 1e-6) / n_bd
     t_comm = 0.0
-    if world > 1:
+    if sg is not None:  # the peer scatter + arrival wait over the plain shard GEMM
+        t_fpra = loop_ms(lambda: sg.step())
+        t_comm = max(t_fpra - t_fpr, 0.0) / n_bd
+    elif world > 1:
         t_fpra = loop_ms(lambda: (runner.launch(stage="prepare"), runner.launch(stage="run"),
                                   part.assemble(runner.y, y_full)))
         t_comm = max(t_fpra - t_fpr, 0.0) / n_bd
@@ -374,7 +432,19 @@ def run_ours(args) -> None:
     Xh = torch.from_numpy(X).pin_memory()
     tb = tg.BiasVector(db)
 
+    h2d_bytes = int(world * M * K * 4)
+    if sg is not None:
+        # the fused path's public surface is ScatterGemm: X (pinned) -> the runners' X buffer,
+        # one step, the assembled Y back to the host on rank 0
+        Xh_in = torch.zeros(tuple(xin.shape), dtype=torch.float32).pin_memory()
+        Xh_in[:, :K] = torch.from_numpy(X)
+        h2d_bytes = int(world * Xh_in.numel() * 4)
+
     def api_call():
+        if sg is not None:
+            xin.copy_(Xh_in, non_blocking=True)
+            y = sg.step()
+            return tg.DenseMatrix(y).values if rank == 0 else None
         if sym:
             y = tg.gemm_vectorized_optimal(tg.pad_input(Xh), fmt, tb, wl.alpha, method=method)
         elif kind == "interleaved_blocked":
@@ -409,6 +479,9 @@ def run_ours(args) -> None:
     if rank != 0:
         if world > 1:
             dist.barrier()
+            if bufs is not None:
+                torch.cuda.synchronize()
+                bufs.close()
             dist.destroy_process_group()
         return
 
@@ -469,22 +542,31 @@ def run_ours(args) -> None:
                "what": "oracle/tg_oracle.c: C restatement of the reference numba kernel, bit-exact with it"}
 
     launches_per_step = 2  # mma: X split + tile MMA; gather: transpose + gather
+    if sg is not None:
+        launches_per_step = 3  # + the arrival wait
     line = {
         "metric": "effective_gops", "value": round(value, 3), "unit": "GOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(t_step_max, 5), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (BASELINE.json recipe, seeded; no dataset)",
         "config": {"workload": cfg, "M": M, "K": K, "N": N, "p_nonzero": wl.p_pos + wl.p_neg, "nnz": nnz_total,
                    "alpha": wl.alpha, "variant": wl.variant, "method": method,
-                   "parallelism": f"N-sharded x{world}" + (" + NCCL all-gather" if world > 1 else ""),
+                   "parallelism": f"N-sharded x{world}" + (
+                       "" if world == 1 else " + fused peer-store epilogue over NVLink" if assembly == "peer"
+                       else " + NCCL all-gather"),
                    "l2": "flushed (256 MB write) before every timed step; step time = (K x (flush+step) - K x flush) / K",
                    "launch": "CUDA graph replay per step" if graph is not None else "direct launches"},
         "breakdown_ms": {"prepare": round(t_prep, 5), "run": round(t_run, 5), "assemble": round(t_comm, 5),
-                         "note": "loop differences over K steps with direct launches; run = GEMM kernel after the split"},
+                         "note": "loop differences over K steps with direct launches; run = GEMM kernel after the "
+                                 "split; assemble = extra time of the shard assembly (NCCL all-gather, or the fused "
+                                 "peer stores + arrival wait)"},
+        "assembly": {"kind": assembly, "note": asm_note},
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_value, 3) if e2e_value else None, "unit": "GOP/s", "ms_per_step": round(t_e2e_ms, 4),
-                "h2d_bytes_per_step": int(world * M * K * 4), "d2h_bytes_per_step": int(M * N * 4),
-                "path": f"public API gemm_* on pinned host X ({'pad_input + ' if sym else ''}{kind}), Y.values"},
+                "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": int(M * N * 4),
+                "path": (f"ScatterGemm.step on pinned host X (H2D into the shard runners' X), rank 0 reads the "
+                         f"assembled Y" if sg is not None else
+                         f"public API gemm_* on pinned host X ({'pad_input + ' if sym else ''}{kind}), Y.values")},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk,
         "parity": {"normwise_vs_fp64": nw},
@@ -492,6 +574,9 @@ def run_ours(args) -> None:
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
+        if bufs is not None:
+            torch.cuda.synchronize()
+            bufs.close()
         dist.destroy_process_group()
 
 
@@ -506,6 +591,8 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the public-API end-to-end leg (profiling runs)")
     ap.add_argument("--no-graph", action="store_true", help="issue the step's kernels one by one instead of a CUDA graph")
+    ap.add_argument("--assembly", default="peer", choices=("peer", "nccl"),
+                    help="N > 1: assemble Y in the GEMM epilogue over NVLink peer memory (default) or NCCL all-gather")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

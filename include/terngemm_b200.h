@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define TG_ABI_VERSION 2
+#define TG_ABI_VERSION 3
 
 typedef enum {
   TG_OK = 0,
@@ -225,6 +225,57 @@ int tg_gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, const u
 int tg_gemm_tiles(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N,
                   const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, const tg_format_ref* exact,
                   void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream);
+
+/* ---------------------------------------------------------------- peer scatter
+ * Column-sharded GEMM whose epilogue writes every finished Y tile straight
+ * into the full-width Y of every rank over NVLink (peer-mapped memory), so
+ * the shard result never takes a separate all-gather (the north star's "one
+ * NCCL all-gather" assembly, partition.py, fused into the producing kernel).
+ *
+ * Peer memory: each rank allocates one buffer with tg_peer_alloc (a 256-byte
+ * signal header followed by its Y slots), exports it with tg_peer_export,
+ * exchanges the 64-byte handles out of band (e.g. torch.distributed
+ * all_gather_object) and maps the others with tg_peer_import.
+ *
+ * Signal header (uint32 words): [0, world) arrival counters, one per source
+ * rank; TG_PEER_DONE_WORD: this rank's CTA completion counter;
+ * TG_PEER_EPOCH_WORD: the epoch the last tg_peer_wait consumed.
+ *
+ * tg_gemm_tiles_run_scatter = tg_gemm_tiles_run with Y = this rank's block
+ * (its columns col_off.. of its own full Y, row pitch ldy); every finished
+ * tile is additionally stored at the same offset into y_peers[q] for q !=
+ * rank; after the last tile of the grid the kernel adds 1 to word `rank` of
+ * every rank's header (system-scope release).  tg_peer_wait (stream-ordered,
+ * one tiny launch) returns once every rank's counter in this rank's header
+ * has reached the next epoch: all shards of this step are then in local HBM.
+ * With two Y slots used alternately, a rank cannot overwrite a peer's slot
+ * before that peer has passed its previous wait.            */
+#define TG_PEER_HEADER_BYTES 256
+#define TG_PEER_MAX_WORLD 32
+#define TG_PEER_DONE_WORD 32
+#define TG_PEER_EPOCH_WORD 33
+#define TG_PEER_TIMEOUT_WORD 34 /* set to 1 by a tg_peer_wait that gave up after ~10 s */
+#define TG_PEER_HANDLE_BYTES 64
+
+typedef struct {
+  float* const* y_peers;      /* device array [world]: Y slot base (column 0, row 0) of every rank */
+  uint32_t* const* sig_peers; /* device array [world]: signal header of every rank */
+  uint32_t* sig_local;        /* this rank's header (== sig_peers[rank]) */
+  int32_t world;
+  int32_t rank;
+  int64_t col_off;            /* first column of this rank's block in the full Y */
+} tg_peer_scatter;
+
+int tg_peer_alloc(size_t bytes, void** ptr);               /* zeroed, cudaIpc-exportable */
+int tg_peer_free(void* ptr);
+int tg_peer_export(void* ptr, void* handle /* TG_PEER_HANDLE_BYTES */);
+int tg_peer_import(const void* handle, void** ptr);        /* maps a peer's buffer */
+int tg_peer_release(void* ptr);                             /* unmaps an imported buffer */
+int tg_peer_wait(uint32_t* sig_local, int world, void* stream);
+int tg_gemm_tiles_run_scatter(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles,
+                              int64_t N, const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha,
+                              const tg_format_ref* exact, const tg_peer_scatter* scatter, void* ws,
+                              size_t ws_bytes, tg_device_flags* flags, void* stream);
 
 #ifdef __cplusplus
 }

@@ -62,6 +62,26 @@ TG_VARIANT_VERTICAL = 5
 TG_VARIANT_HORIZONTAL = 6
 TG_VARIANT_COMPRESSED = 7
 
+TG_PEER_HEADER_BYTES = 256
+TG_PEER_MAX_WORLD = 32
+TG_PEER_DONE_WORD = 32
+TG_PEER_EPOCH_WORD = 33
+TG_PEER_TIMEOUT_WORD = 34
+TG_PEER_HANDLE_BYTES = 64
+
+
+class TgPeerScatter(ctypes.Structure):
+    """tg_peer_scatter: peer tables of a fused column-shard scatter (device arrays)."""
+
+    _fields_ = [
+        ("y_peers", ctypes.c_void_p),
+        ("sig_peers", ctypes.c_void_p),
+        ("sig_local", ctypes.c_void_p),
+        ("world", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("col_off", ctypes.c_int64),
+    ]
+
 
 class TgFormatRef(ctypes.Structure):
     _fields_ = [
@@ -127,6 +147,16 @@ SIGNATURES: dict[str, tuple] = {
     "tg_gemm_tiles_prepare": (_I, [_P, _I64, _I64, _I64, _P, _SZ, _P, _P]),
     "tg_gemm_tiles_run": (_I, [_P, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _I, _F, _P, _P, _SZ, _P, _P]),
     "tg_gemm_tiles": (_I, [_P, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _I, _F, _P, _P, _SZ, _P, _P]),
+    "tg_peer_alloc": (_I, [_SZ, ctypes.POINTER(_P)]),
+    "tg_peer_free": (_I, [_P]),
+    "tg_peer_export": (_I, [_P, _P]),
+    "tg_peer_import": (_I, [_P, ctypes.POINTER(_P)]),
+    "tg_peer_release": (_I, [_P]),
+    "tg_peer_wait": (_I, [_P, _I, _P]),
+    "tg_gemm_tiles_run_scatter": (
+        _I,
+        [_P, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _I, _F, _P, ctypes.POINTER(TgPeerScatter), _P, _SZ, _P, _P],
+    ),
 }
 
 _lock = threading.Lock()

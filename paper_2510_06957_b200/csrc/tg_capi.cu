@@ -168,9 +168,10 @@ int tg_gemm_tiles_prepare(const float* X, int64_t M, int64_t K, int64_t ldx, voi
   return run_xsplit(X, M, K, ldx, ws, ws_bytes, flags, as_stream(stream));
 }
 
-int tg_gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N,
-                      const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, const tg_format_ref* exact,
-                      void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream) {
+static int gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N,
+                          const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha,
+                          const tg_format_ref* exact, const tg_peer_scatter* sc, void* ws, size_t ws_bytes,
+                          tg_device_flags* flags, void* stream) {
   TG_REQUIRE(M >= 1 && K >= 1 && N >= 1, TG_ERR_PARAM, "M, K and N must be >= 1");
   TG_REQUIRE(ldy >= N && ldx >= K, TG_ERR_PARAM, "leading dimensions too small");
   TG_REQUIRE(tiles && Y && ws && X, TG_ERR_PARAM, "null pointer");
@@ -187,7 +188,7 @@ int tg_gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, const u
   TG_REQUIRE(ws_bytes >= mma_ws_bytes(M, K, N), TG_ERR_PARAM, "workspace too small");
   TG_TRY(require_device());
   if (!exact) return run_mma(X, M, K, ldx, tiles, N, bias, Y, ldy, use_alpha, alpha, nullptr, ws, ws_bytes, flags,
-                             as_stream(stream));
+                             as_stream(stream), sc);
   const int v = exact->variant;
   MmaFixup fx{};
   const int64_t nb = (v == TG_VARIANT_BASE || v == TG_VARIANT_UNROLLED) ? 1 : ceil_div(K, exact->B);
@@ -207,7 +208,78 @@ int tg_gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, const u
                          v == TG_VARIANT_BASE ? 1 : exact->uf, nullptr, 0};
   }
   return run_mma(X, M, K, ldx, tiles, N, bias, Y, ldy, use_alpha, alpha, &fx, ws, ws_bytes, flags,
-                 as_stream(stream));
+                 as_stream(stream), sc);
+}
+
+int tg_gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N,
+                      const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, const tg_format_ref* exact,
+                      void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream) {
+  return gemm_tiles_run(X, M, K, ldx, tiles, N, bias, Y, ldy, use_alpha, alpha, exact, nullptr, ws, ws_bytes, flags,
+                        stream);
+}
+
+int tg_gemm_tiles_run_scatter(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles,
+                              int64_t N, const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha,
+                              const tg_format_ref* exact, const tg_peer_scatter* scatter, void* ws,
+                              size_t ws_bytes, tg_device_flags* flags, void* stream) {
+  TG_REQUIRE(scatter, TG_ERR_PARAM, "null scatter descriptor");
+  TG_REQUIRE(scatter->world >= 1 && scatter->world <= TG_PEER_MAX_WORLD, TG_ERR_PARAM,
+             "scatter world must be in [1, TG_PEER_MAX_WORLD]");
+  TG_REQUIRE(scatter->rank >= 0 && scatter->rank < scatter->world, TG_ERR_PARAM, "scatter rank out of range");
+  TG_REQUIRE(scatter->y_peers && scatter->sig_peers && scatter->sig_local, TG_ERR_PARAM,
+             "scatter descriptor with null tables");
+  TG_REQUIRE(scatter->col_off >= 0 && scatter->col_off + N <= ldy, TG_ERR_PARAM,
+             "scatter block [col_off, col_off + N) must lie inside the full row pitch ldy");
+  return gemm_tiles_run(X, M, K, ldx, tiles, N, bias, Y, ldy, use_alpha, alpha, exact, scatter, ws, ws_bytes, flags,
+                        stream);
+}
+
+// ------------------------------------------------------------------ peer memory
+int tg_peer_alloc(size_t bytes, void** ptr) {
+  TG_REQUIRE(ptr && bytes > 0, TG_ERR_PARAM, "tg_peer_alloc: null output or zero size");
+  TG_TRY(require_device());
+  *ptr = nullptr;
+  cudaError_t e = cudaMalloc(ptr, bytes);  // its own allocation: cudaIpc exports whole allocations
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaMalloc(peer buffer)");
+  e = cudaMemset(*ptr, 0, bytes);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaMemset(peer buffer)");
+  return TG_OK;
+}
+
+int tg_peer_free(void* ptr) {
+  cudaError_t e = cudaFree(ptr);
+  return e == cudaSuccess ? TG_OK : set_cuda_error(e, "cudaFree(peer buffer)");
+}
+
+int tg_peer_export(void* ptr, void* handle) {
+  TG_REQUIRE(ptr && handle, TG_ERR_PARAM, "tg_peer_export: null pointer");
+  static_assert(sizeof(cudaIpcMemHandle_t) == TG_PEER_HANDLE_BYTES, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, ptr);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaIpcGetMemHandle");
+  memcpy(handle, &h, sizeof(h));
+  return TG_OK;
+}
+
+int tg_peer_import(const void* handle, void** ptr) {
+  TG_REQUIRE(ptr && handle, TG_ERR_PARAM, "tg_peer_import: null pointer");
+  TG_TRY(require_device());
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? TG_OK : set_cuda_error(e, "cudaIpcOpenMemHandle");
+}
+
+int tg_peer_release(void* ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  return e == cudaSuccess ? TG_OK : set_cuda_error(e, "cudaIpcCloseMemHandle");
+}
+
+int tg_peer_wait(uint32_t* sig_local, int world, void* stream) {
+  TG_REQUIRE(sig_local, TG_ERR_PARAM, "tg_peer_wait: null header");
+  TG_REQUIRE(world >= 1 && world <= TG_PEER_MAX_WORLD, TG_ERR_PARAM, "world must be in [1, TG_PEER_MAX_WORLD]");
+  TG_TRY(require_device());
+  return run_peer_wait(sig_local, world, as_stream(stream));
 }
 
 int tg_gemm_tiles(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N,

@@ -30,6 +30,9 @@ int run_pack_csc(const int32_t* col_start, const int32_t* rows, int64_t N, int64
 int run_pack_ib(const int32_t* ai, const int32_t* ptr, int64_t N, int64_t nblocks, int g, int64_t K,
                 uint32_t* tiles, tg_device_flags* flags, cudaStream_t st);
 
+// tg_peer.cu
+int run_peer_wait(uint32_t* sig, int world, cudaStream_t st);
+
 int run_unpack_dense(const uint32_t* tiles, int64_t K, int64_t N, int8_t* W, cudaStream_t st);
 
 // tg_gather.cu
@@ -60,5 +63,5 @@ int run_pack_sym(const int32_t* idx, const int32_t* ptr, int64_t N, int g, int64
 int run_pack_codes(const uint8_t* codes, int64_t K, int64_t N, uint32_t* tiles, cudaStream_t st);
 int run_mma(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N, const float* bias,
             float* Y, int64_t ldy, int use_alpha, float alpha, const MmaFixup* fix, void* ws, size_t ws_bytes,
-            tg_device_flags* flags, cudaStream_t st);
+            tg_device_flags* flags, cudaStream_t st, const tg_peer_scatter* sc = nullptr);
 }  // namespace tg

@@ -385,7 +385,21 @@ struct MmaParams {
   const float* X;          // original X (fix-up reads it in place)
   int64_t ldx;
   int tma_y;               // 1: Y tiles leave through smem + TMA store (ymap), 0: direct stores
+  // peer scatter (tg_gemm_tiles_run_scatter): every finished tile also goes to
+  // ypeers[q] + col_off + m * ldy + n for q != rank; sig_local == null: off
+  float* const* ypeers;
+  uint32_t* const* speers;
+  uint32_t* sig_local;
+  int world, rank;
+  int64_t col_off;
 };
+
+// One Y row segment to every other rank's full Y (plain st.global over NVLink).
+__device__ __forceinline__ void peer_store(const MmaParams& p, int64_t off, float y) {
+#pragma unroll 1
+  for (int q = 0; q < p.world; ++q)
+    if (q != p.rank) p.ypeers[q][off] = y;
+}
 
 // Tile configuration.  A pipeline stage covers 256 k (two 128-k chunks: 8
 // MMAs of K = 32 and ONE tcgen05.commit -- a commit costs about as much as an
@@ -467,6 +481,7 @@ struct EmitCtx {
   uint32_t ysmem;
   float* ydst;       // false: Y (row stride ldy)
   int64_t ystride;
+  int64_t yoff;      // element offset of ydst in this rank's full Y (peer scatter)
 };
 
 __device__ __forceinline__ void load_scales(uint32_t addr, float4 (&sc)[16]) {
@@ -539,6 +554,43 @@ __device__ __forceinline__ void emit_tail(float (&v)[16], const long long* tot_o
 #pragma unroll
     for (int j = 0; j < 16; ++j)
       if (j < e.nvalid) e.ydst[int64_t(j) * e.ystride] = v[j];
+  }
+  if (p.sig_local) {
+#pragma unroll 1
+    for (int q = 0; q < p.world; ++q) {
+      if (q == p.rank) continue;
+      float* d = p.ypeers[q] + e.yoff;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < e.nvalid) d[int64_t(j) * e.ystride] = v[j];
+    }
+  }
+}
+
+// A finished smem Y tile (MT x 128, row pitch 512 B) to every other rank:
+// each warp stores whole 512-byte row segments with 16-byte stores.
+template <int MT>
+__device__ __forceinline__ void peer_copy_tile(const MmaParams& p, const float* ytile, int m0, int n0, int et,
+                                               int nthreads) {
+  const int rows = min(MT, p.M - m0), cols = min(128, p.N - n0);
+#pragma unroll 1
+  for (int i = et; i < rows * 32; i += nthreads) {
+    const int r = i >> 5, c = (i & 31) * 4;
+    if (c >= cols) continue;
+    const float4 v = *reinterpret_cast<const float4*>(ytile + r * 128 + c);
+    const int64_t off = p.col_off + int64_t(m0 + r) * p.ldy + n0 + c;
+#pragma unroll 1
+    for (int q = 0; q < p.world; ++q) {
+      if (q == p.rank) continue;
+      float* d = p.ypeers[q] + off;
+      if (c + 4 <= cols) {
+        *reinterpret_cast<float4*>(d) = v;
+      } else {
+        d[0] = v.x;
+        if (c + 1 < cols) d[1] = v.y;
+        if (c + 2 < cols) d[2] = v.z;
+      }
+    }
   }
 }
 
@@ -854,6 +906,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
         e.ysmem = smem_u32(ytile) + uint32_t(mm * C::BN + c) * 4u;
         e.ydst = p.Y + int64_t(m0 + mm) * p.ldy + n;
         e.ystride = p.ldy;
+        e.yoff = p.col_off + int64_t(m0 + mm) * p.ldy + n;
         return e;
       };
 #pragma unroll 1
@@ -937,8 +990,12 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
               ++npos;
             }
             any_bad |= !isfinite(y);
-            if (p.tma_y) ytile[j * C::BN + c] = y;
-            else p.Y[int64_t(m) * p.ldy + n] = y;
+            if (p.tma_y) {
+              ytile[j * C::BN + c] = y;
+            } else {
+              p.Y[int64_t(m) * p.ldy + n] = y;
+              if (p.sig_local) peer_store(p, p.col_off + int64_t(m) * p.ldy + n, y);
+            }
           }
         }
       }
@@ -949,9 +1006,25 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
           tma_store_2d(&ymap, ytile, n0, m0);
           bulk_commit_group();
         }
+        if (p.sig_local) peer_copy_tile<MT>(p, ytile, m0, n0, et, ET);  // overlaps the local TMA store
       }
     }
     if (et == 0 && p.tma_y) bulk_wait_group0();
+    if (p.sig_local) {
+      // the last CTA to finish tells every rank that this rank's shard is in place
+      __threadfence_system();  // this thread's peer stores before the CTA's arrival
+      named_bar_sync(1, ET);
+      if (et == 0) {
+        const unsigned old = atomicAdd(p.sig_local + TG_PEER_DONE_WORD, 1u);
+        if (old == gridDim.x - 1) {
+          p.sig_local[TG_PEER_DONE_WORD] = 0u;  // every CTA has arrived: reset for the next launch
+          __threadfence_system();
+#pragma unroll 1
+          for (int q = 0; q < p.world; ++q)
+            asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p.speers[q] + p.rank) : "memory");
+        }
+      }
+    }
     if (et == 0) TG_STAMP(7, 3 + 2 * (lu - 1));
     if (et == 0) TG_GT(6);
     if (p.flags) {
@@ -1351,7 +1424,7 @@ static int launch_mma(const CUtensorMap& map, const CUtensorMap& ymap, const Mma
 
 int run_mma(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N, const float* bias,
             float* Y, int64_t ldy, int use_alpha, float alpha, const MmaFixup* fix, void* ws, size_t ws_bytes,
-            tg_device_flags* flags, cudaStream_t st) {
+            tg_device_flags* flags, cudaStream_t st, const tg_peer_scatter* sc) {
   const SplitLayout L = split_layout(M, K, N);
   if (ws_bytes < L.total) return set_error(TG_ERR_PARAM, "workspace too small for the tensor-core path");
   uint8_t* base = static_cast<uint8_t*>(ws);
@@ -1373,7 +1446,9 @@ int run_mma(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* t
   CUtensorMap ymap;
   memset(&ymap, 0, sizeof(ymap));
   int tma_y = 0;
-  if ((reinterpret_cast<uintptr_t>(Y) & 15) == 0 && (ldy * 4) % 16 == 0 && !getenv("TG_MMA_DIRECT_Y")) {
+  // (the peer copy of a scattered tile reuses that alignment: 16-byte stores need col_off % 4 == 0)
+  if ((reinterpret_cast<uintptr_t>(Y) & 15) == 0 && (ldy * 4) % 16 == 0 && !getenv("TG_MMA_DIRECT_Y") &&
+      !(sc && sc->col_off % 4 != 0)) {
     cuuint64_t ydim[2] = {cuuint64_t(N), cuuint64_t(M)};
     cuuint64_t ystride[1] = {cuuint64_t(ldy) * 4};
     cuuint32_t ybox[2] = {128u, cuuint32_t(L.mt)};
@@ -1411,6 +1486,14 @@ int run_mma(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* t
     p.fix = fix->args;
     p.X = X;
     p.ldx = ldx;
+  }
+  if (sc) {
+    p.ypeers = sc->y_peers;
+    p.speers = sc->sig_peers;
+    p.sig_local = sc->sig_local;
+    p.world = sc->world;
+    p.rank = sc->rank;
+    p.col_off = sc->col_off;
   }
   if (L.splits > 1) {
     p.counters = reinterpret_cast<int32_t*>(base + L.off_counters);

@@ -228,7 +228,7 @@ class GemmRunner:
 
     def __init__(self, kind: str, x: torch.Tensor, fmt, bias: torch.Tensor, *, method: str, uf: int = 1,
                  mr: int = 1, alpha: float | None = None, out: torch.Tensor | None = None,
-                 flags: torch.Tensor | None = None):
+                 flags: torch.Tensor | None = None, scatter: "nat.TgPeerScatter | None" = None):
         self.kind = kind
         self.x = x
         self.fmt = fmt
@@ -240,6 +240,12 @@ class GemmRunner:
         self.method = method
         dev = x.device
         self.y = out if out is not None else torch.empty((self.M, self.N), dtype=torch.float32, device=dev)
+        if tuple(self.y.shape) != (self.M, self.N) or self.y.dtype != torch.float32 or self.y.stride(1) != 1:
+            raise ParameterError(f"out must be a float32 [{self.M}, {self.N}] view with unit column stride")
+        self.ldy = int(self.y.stride(0))  # a column block of a wider Y (peer scatter) has ldy > N
+        self.scatter = scatter
+        if scatter is not None and method != "mma":
+            raise ParameterError("the peer scatter is fused into the tensor-core epilogue: method must be 'mma'")
         self.flags = flags if flags is not None else torch.zeros(6, dtype=torch.int32, device=dev)
         self.ws_bytes = nat.load().tg_gemm_workspace_bytes(self.M, self.K, self.N)
         self.tiles = fmt.tiles() if method == "mma" else None
@@ -283,30 +289,36 @@ class GemmRunner:
             if stage in ("all", "prepare"):
                 nat.call("tg_gemm_tiles_prepare", x, M, K, ldx, _p(ws), ws.numel(), fl, st)
             if stage in ("all", "run"):
-                nat.call("tg_gemm_tiles_run", x, M, K, ldx, _p(self.tiles), N, b, y, N, self.use_alpha, self.alpha,
-                         ctypes.byref(self.exact), _p(ws), ws.numel(), fl, st)
+                if self.scatter is not None:
+                    nat.call("tg_gemm_tiles_run_scatter", x, M, K, ldx, _p(self.tiles), N, b, y, self.ldy,
+                             self.use_alpha, self.alpha, ctypes.byref(self.exact), ctypes.byref(self.scatter),
+                             _p(ws), ws.numel(), fl, st)
+                else:
+                    nat.call("tg_gemm_tiles_run", x, M, K, ldx, _p(self.tiles), N, b, y, self.ldy, self.use_alpha,
+                             self.alpha, ctypes.byref(self.exact), _p(ws), ws.numel(), fl, st)
             return
         if stage == "prepare":
             return
         if self.kind in ("vertical", "horizontal"):
             order = nat.TG_ORDER_VERTICAL if self.kind == "vertical" else nat.TG_ORDER_HORIZONTAL
             nat.call("tg_gemm_symmetric", x, M, K, ldx, f.g, _p(f.device("indices")), _p(f.device("col_ptr")), N, b,
-                     y, N, order, self.use_alpha, self.alpha, _p(ws), ws.numel(), fl, st)
+                     y, self.ldy, order, self.use_alpha, self.alpha, _p(ws), ws.numel(), fl, st)
         elif self.kind == "compressed":
-            nat.call("tg_gemm_compressed", x, M, K, ldx, _p(f.device()), N, b, y, N, _p(ws), ws.numel(), fl, st)
+            nat.call("tg_gemm_compressed", x, M, K, ldx, _p(f.device()), N, b, y, self.ldy, _p(ws), ws.numel(), fl,
+                     st)
         elif self.kind in ("base", "unrolled"):
             nat.call("tg_gemm_tcsc", x, M, K, ldx, _p(f.device("col_start_pos")), _p(f.device("row_index_pos")),
-                     _p(f.device("col_start_neg")), _p(f.device("row_index_neg")), N, b, y, N,
+                     _p(f.device("col_start_neg")), _p(f.device("row_index_neg")), N, b, y, self.ldy,
                      0 if self.kind == "base" else self.uf, self.use_alpha, self.alpha, _p(ws), ws.numel(), fl, st)
         elif self.kind == "blocked":
             nat.call("tg_gemm_blocked", x, M, K, ldx, f.B, _p(f.device("col_start_pos")),
                      _p(f.device("row_index_pos")), _p(f.device("col_start_neg")), _p(f.device("row_index_neg")), N,
-                     b, y, N, self.uf, self.mr, self.use_alpha, self.alpha, _p(ws), ws.numel(), fl, st)
+                     b, y, self.ldy, self.uf, self.mr, self.use_alpha, self.alpha, _p(ws), ws.numel(), fl, st)
         else:
             order = (nat.TG_ORDER_VECTORIZED_OPTIMAL if self.kind == "vectorized_optimal"
                      else nat.TG_ORDER_INTERLEAVED_BLOCKED)
             nat.call("tg_gemm_interleaved_blocked", x, M, K, ldx, f.B, f.g, _p(f.device("all_indices")),
-                     _p(f.device("col_segment_ptr")), N, b, y, N, order, self.use_alpha, self.alpha, _p(ws),
+                     _p(f.device("col_segment_ptr")), N, b, y, self.ldy, order, self.use_alpha, self.alpha, _p(ws),
                      ws.numel(), fl, st)
 
     def capture(self, warmup: bool = True) -> "torch.cuda.CUDAGraph":
