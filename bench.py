@@ -291,7 +291,8 @@ def run_ours(args) -> None:
     # ---- shard assembly (N > 1): the fused peer-store epilogue by default, NCCL on request
     assembly = "none" if world == 1 else args.assembly
     asm_note = None
-    if assembly == "peer" and method != "mma":
+    # (agreed over ranks: every rank must take the same assembly)
+    if assembly == "peer" and max_over_ranks(0.0 if method == "mma" else 1.0, world, dev) != 0.0:
         assembly, asm_note = "nccl", "gather method has no fused epilogue; NCCL all-gather"
     sg = bufs = None
     if assembly == "peer":

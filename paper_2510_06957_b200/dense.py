@@ -128,6 +128,13 @@ class TernaryDense:
         return f"TernaryDense(K={self.K}, N={self.N})"
 
 
+def _flags_bad(f) -> bool:
+    """Kernel status words (tg_device_flags as int32): a non-finite output, or a
+    non-finite X entry seen by the tensor-core split (bad_input bit 2; the
+    reference rejects such an X when it is constructed, dense.py:77)."""
+    return int(f[1]) != 0 or (int(f[0]) & 4) != 0
+
+
 class DenseMatrix:
     """Row-major float32 matrix with all entries finite (dense.py:67-90).
 
@@ -159,7 +166,7 @@ class DenseMatrix:
     def check(self) -> "DenseMatrix":
         if not self._checked:
             if self._flags is not None:
-                bad = int(self._flags[1].item()) != 0
+                bad = _flags_bad(self._flags.cpu().numpy())
             else:
                 bad = not bool(torch.isfinite(self._v._d).all().item())
             if bad:
@@ -173,7 +180,7 @@ class DenseMatrix:
         if v._h is None and not self._checked and self._flags is not None and v._d is not None and v._d.is_cuda:
             # fetch Y and the kernel's status words with one synchronisation
             h, f = _to_host(v._d.detach(), self._flags)
-            if int(f[1]) != 0:
+            if _flags_bad(f):
                 raise ParameterError("dense matrix contains non-finite values")
             self._checked = True
             v._h = h

@@ -118,3 +118,17 @@ def test_wide_rows_without_exact_format_use_fp64(tg):
         den = ref[m].abs().max()
         err = float((y[m].double() - ref[m]).abs().max() / den) if den > 0 else float(y[m].abs().max())
         assert err <= TOL, (m, err)
+
+
+def test_nonfinite_input_is_reported(tg):
+    """A non-finite X entry (the reference rejects it when constructing DenseMatrix,
+    dense.py:77) is flagged by the tensor-core split and raised on first host access."""
+    from paper_2510_06957_b200.errors import ParameterError
+
+    M, K, N = 20, 256, 128
+    W = torch.randint(-1, 2, (K, N), device="cuda", dtype=torch.int8)
+    X = torch.randn((M, K), device="cuda")
+    X[5, 7] = float("inf")
+    t = tg.tcsc_from_dense(tg.TernaryDense(W))
+    with pytest.raises(ParameterError):
+        tg.gemm_base(X, t, torch.zeros(N, device="cuda"), method="mma").values
