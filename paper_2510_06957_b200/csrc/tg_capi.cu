@@ -4,9 +4,13 @@
 // tg_build.cu (format builders), tg_gather.cu (CUDA-core gather path) and
 // tg_mma.cu (dense-decode tensor-core path).
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "tg_internal.h"
 
@@ -30,14 +34,17 @@ int check_launch(const char* where) {
 }
 
 static int require_device() {
+  static std::atomic<uint64_t> ok_mask{0};  // devices already checked (ids < 64)
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return set_cuda_error(e, "cudaGetDevice");
+  if (dev < 64 && (ok_mask.load(std::memory_order_relaxed) >> dev) & 1u) return TG_OK;
   int major = 0, minor = 0;
   cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
   cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
   if (major != 10 || minor != 0)
     return set_error(TG_ERR_UNSUPPORTED, "terngemm_b200 is built for sm_100a (B200) only");
+  if (dev < 64) ok_mask.fetch_or(uint64_t(1) << dev, std::memory_order_relaxed);
   return TG_OK;
 }
 
@@ -288,6 +295,127 @@ int tg_gemm_tiles(const float* X, int64_t M, int64_t K, int64_t ldx, const uint3
   TG_TRY(tg_gemm_tiles_prepare(X, M, K, ldx, ws, ws_bytes, flags, stream));
   return tg_gemm_tiles_run(X, M, K, ldx, tiles, N, bias, Y, ldy, use_alpha, alpha, exact, ws, ws_bytes, flags,
                            stream);
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ GEMM from host memory
+namespace {
+
+// Row chunks of a host-resident X: about 2 MB of X each (a chunk's PCIe time,
+// ~40 us, must cover the ~25 us of host work to enqueue the next one), at most
+// 8, starting at multiples of 64 rows (a multiple of every blocked-order row
+// unroll mr).
+struct HostPlan {
+  int64_t rows, n;  // chunk height (the last one may be shorter), chunk count
+  int streams;      // side streams used
+  size_t ws_slice;  // workspace per side stream
+};
+
+HostPlan host_plan(int64_t M, int64_t K, int64_t N) {
+  HostPlan P;
+  const int64_t bytes = M * K * 4;
+  int64_t cap = 8;
+  if (const char* env = getenv("TG_HOST_CHUNKS")) cap = std::max(1, atoi(env));
+  int64_t n = std::max<int64_t>(1, std::min<int64_t>({cap, bytes >> 21, M / 64}));
+  P.rows = round_up(ceil_div(M, n), 64);
+  P.n = ceil_div(M, P.rows);
+  P.streams = int(std::min<int64_t>(P.n, 4));
+  const int64_t last = M - (P.n - 1) * P.rows;
+  P.ws_slice = size_t(round_up(int64_t(std::max(mma_ws_bytes(P.rows, K, N), mma_ws_bytes(last, K, N))), 256));
+  return P;
+}
+
+// The library's own side streams and events, per device (created once).
+struct SideStreams {
+  cudaStream_t s[4];
+  cudaEvent_t join[4];
+  cudaEvent_t fork;
+};
+
+int side_streams(SideStreams** out) {
+  static std::mutex mu;
+  static std::unordered_map<int, SideStreams> per_dev;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = per_dev.find(dev);
+  if (it == per_dev.end()) {
+    SideStreams ss;
+    for (int i = 0; i < 4; ++i) {
+      if ((e = cudaStreamCreateWithFlags(&ss.s[i], cudaStreamNonBlocking)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&ss.join[i], cudaEventDisableTiming)) != cudaSuccess)
+        return set_cuda_error(e, "side stream creation");
+    }
+    if ((e = cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming)) != cudaSuccess)
+      return set_cuda_error(e, "side stream creation");
+    it = per_dev.emplace(dev, ss).first;
+  }
+  *out = &it->second;
+  return TG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t tg_gemm_host_workspace_bytes(int64_t M, int64_t K, int64_t N) {
+  if (M < 1 || K < 1 || N < 1) return 0;
+  const HostPlan P = host_plan(M, K, N);
+  return size_t(P.streams) * P.ws_slice;
+}
+
+int tg_gemm_tiles_host(const float* X_host, int64_t M, int64_t K, int64_t ldx_host, float* X_dev, int64_t ldx_dev,
+                       const uint32_t* tiles, int64_t N, const float* bias, float* Y_dev, int64_t ldy_dev,
+                       float* Y_host, int64_t ldy_host, int use_alpha, float alpha, const tg_format_ref* exact,
+                       void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream) {
+  TG_REQUIRE(M >= 1 && K >= 1 && N >= 1, TG_ERR_PARAM, "M, K and N must be >= 1");
+  TG_REQUIRE(X_host && X_dev && Y_dev && Y_host && tiles && ws, TG_ERR_PARAM, "null pointer");
+  TG_REQUIRE(ldx_host >= K && ldx_dev >= K && ldy_dev >= N && ldy_host >= N, TG_ERR_PARAM,
+             "leading dimensions too small");
+  TG_REQUIRE(ws_bytes >= tg_gemm_host_workspace_bytes(M, K, N), TG_ERR_PARAM, "workspace too small");
+  TG_TRY(require_device());
+  const HostPlan P = host_plan(M, K, N);
+  SideStreams* ss = nullptr;
+  TG_TRY(side_streams(&ss));
+  static std::mutex enqueue_mu;  // the side streams and their events are shared by every caller
+  std::lock_guard<std::mutex> lk(enqueue_mu);
+  cudaStream_t main = as_stream(stream);
+  cudaError_t e;
+  if (ldx_dev > K) {  // the padded input's slot column(s): zero, as pad_input does
+    e = cudaMemset2DAsync(X_dev + K, size_t(ldx_dev) * 4, 0, size_t(ldx_dev - K) * 4, size_t(M), main);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaMemset2DAsync(padded slot)");
+  }
+  if ((e = cudaEventRecord(ss->fork, main)) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
+  for (int i = 0; i < P.streams; ++i)
+    if ((e = cudaStreamWaitEvent(ss->s[i], ss->fork, 0)) != cudaSuccess) return set_cuda_error(e, "fork");
+  for (int64_t c = 0; c < P.n; ++c) {
+    const int i = int(c % P.streams);
+    cudaStream_t st = ss->s[i];
+    const int64_t r0 = c * P.rows, rows = std::min(P.rows, M - r0);
+    float* xd = X_dev + r0 * ldx_dev;
+    float* yd = Y_dev + r0 * ldy_dev;
+    void* wsi = static_cast<uint8_t*>(ws) + size_t(i) * P.ws_slice;
+    e = ldx_dev == K && ldx_host == K
+            ? cudaMemcpyAsync(xd, X_host + r0 * K, size_t(rows * K) * 4, cudaMemcpyHostToDevice, st)
+            : cudaMemcpy2DAsync(xd, size_t(ldx_dev) * 4, X_host + r0 * ldx_host, size_t(ldx_host) * 4,
+                                size_t(K) * 4, size_t(rows), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaMemcpy2DAsync(X chunk)");
+    TG_TRY(tg_gemm_tiles_prepare(xd, rows, K, ldx_dev, wsi, P.ws_slice, flags, st));
+    TG_TRY(gemm_tiles_run(xd, rows, K, ldx_dev, tiles, N, bias, yd, ldy_dev, use_alpha, alpha, exact, nullptr, wsi,
+                          P.ws_slice, flags, st));
+    e = ldy_dev == N && ldy_host == N
+            ? cudaMemcpyAsync(Y_host + r0 * N, yd, size_t(rows * N) * 4, cudaMemcpyDeviceToHost, st)
+            : cudaMemcpy2DAsync(Y_host + r0 * ldy_host, size_t(ldy_host) * 4, yd, size_t(ldy_dev) * 4,
+                                size_t(N) * 4, size_t(rows), cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaMemcpy2DAsync(Y chunk)");
+  }
+  for (int i = 0; i < P.streams; ++i) {
+    if ((e = cudaEventRecord(ss->join[i], ss->s[i])) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
+    if ((e = cudaStreamWaitEvent(main, ss->join[i], 0)) != cudaSuccess) return set_cuda_error(e, "join");
+  }
+  return TG_OK;
 }
 
 }  // extern "C"

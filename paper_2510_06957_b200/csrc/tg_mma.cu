@@ -6,30 +6,30 @@
 // i.e. Y[m,n] = b[n] + sum_{k: W[k,n]=+1} X[m,k] - sum_{k: W[k,n]=-1} X[m,k],
 // then y <- (y > 0 ? y : alpha*y) in fp32 when PReLU is on (simd.py:410-417).
 //
-// Realisation (B200-native, see DESIGN.md "dense-decode path"):
-//   1. tg_xsplit_kernel: each X row is staged once in shared memory, scaled by
-//      a power of two 2^s so that max|x| < 2^22, rounded to an integer v, and v
-//      is split into three balanced signed base-256 digits (int8 "limbs").
-//      Exact for integer X.
+// Realisation (B200-native, see DESIGN.md section 3.1):
+//   1. tg_xsplit_*_kernel: each X row is scaled by a power of two 2^s so that
+//      max|x| < 2^22, rounded to an integer v, and v is split into three
+//      balanced signed base-256 digits (int8 "limbs").  Exact for integer X.
+//      Rows whose nonzeros span a wide dynamic range are marked "wide".
 //   2. tg_mma_kernel: persistent, warp-specialised, one CTA per SM.  A work
 //      unit is (128 output columns) x (MT output rows) x (a K range):
-//        warp 0    TMA: the three limb tiles of X (SWIZZLE_128B) and the
-//                  packed 2-bit ternary tile of W (one 4 KB bulk copy) per stage
-//        warps 2-5 decode the packed tile in shared memory into int8 {-1,0,+1}
-//                  K-major SW128 tiles (the "expanded ternary tile")
-//        warp 1    one elected lane issues tcgen05.mma.kind::i8 with
-//                  A = W^T tile (M=128 rows = output columns n),
-//                  B = [limb0; limb1; limb2] (N = 3*MT rows = output rows m)
-//                  into one of two int32 TMEM accumulators (double-buffered so
-//                  the epilogue of a unit overlaps the MMAs of the next).
-//                  Integer accumulation is exact: the result does not depend
-//                  on summation order, so K may be split across CTAs.
-//        warps 6-9 epilogue: tcgen05.ld the three limb sums, recombine exactly
-//                  in int64, scale by 2^-s in fp64, add the bias, round once to
-//                  fp32, PReLU, coalesced store of Y.  Split-K units write
-//                  int64 partials; the last unit of a tile reduces them.
-//                  Rows flagged "wide" by the split (negative scale) are then recomputed in the
-//                  reference's exact operation order (tg_walk.cuh).
+//        warp 0     TMA: the three limb tiles of X (SWIZZLE_128B), multicast
+//                   across a cluster of 1/2/4 CTAs sharing the rows
+//        warp 6     bulk copies of the packed 2-bit ternary W tiles (own ring)
+//        warps 2-5  decode the packed tile into int8 {-1,0,+1} W^T rows and
+//                   write them straight into TMEM (tcgen05.st)
+//        warp 1     one lane issues tcgen05.mma.kind::i8, A = W^T from TMEM,
+//                   B = [limb0; limb1; limb2] from smem (N = 3*MT), into one of
+//                   two int32 TMEM accumulators (the epilogue of a unit
+//                   overlaps the MMAs of the next).  Integer accumulation is
+//                   exact and order-independent, so K may be split across CTAs.
+//        warps 7-14 epilogue: tcgen05.ld the three limb sums, recombine them with
+//                   three fp32 FMAs (exact for integer X), add the bias, PReLU,
+//                   st.shared into the Y tile, one TMA store per unit.  Split-K
+//                   units write per-limb int32 partials; the last unit of a tile
+//                   sums them and takes the same epilogue.  Rows marked "wide"
+//                   are then recomputed in the reference's exact operation
+//                   order (tg_walk.cuh).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -376,7 +376,7 @@ struct MmaParams {
   int units;               // cluster units = MB * NBG * splits
   int use_alpha;
   float alpha;
-  long long* part;         // split-K partials [splits][M_pad][N_pad] (splits > 1)
+  int32_t* part;           // split-K limb partials [splits][3][M_pad][N_pad] (splits > 1)
   int32_t* counters;       // [MB * NB] arrival counters, zero between launches
   tg_device_flags* flags;
   int fix_var;             // < 0: no exact-order fix-up of wide rows
@@ -493,18 +493,17 @@ __device__ __forceinline__ void load_scales(uint32_t addr, float4 (&sc)[16]) {
 }
 
 // tail shared by both emitters: PReLU, PReLU count, finiteness, the rare fp64 rows, store
-__device__ __forceinline__ void emit_tail(float (&v)[16], const long long* tot_or_null, const uint32_t* r0,
-                                          const uint32_t* r1, const uint32_t* r2, const EmitCtx& e,
-                                          const MmaParams& p, unsigned long long& npos, bool& bad) {
+__device__ __forceinline__ void emit_tail(float (&v)[16], const uint32_t* r0, const uint32_t* r1, const uint32_t* r2,
+                                          const EmitCtx& e, const MmaParams& p, unsigned long long& npos,
+                                          bool& bad) {
   const bool fix = p.fix_var >= 0;
   if (!fix && e.wide_bits) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       if (((e.wide_bits >> j) & 1u) && j < e.nlive) {
-        const long long t = tot_or_null ? tot_or_null[j]
-                                        : (static_cast<long long>(static_cast<int>(r0[j])) << 16) +
-                                              (static_cast<long long>(static_cast<int>(r1[j])) << 8) +
-                                              static_cast<long long>(static_cast<int>(r2[j]));
+        const long long t = (static_cast<long long>(static_cast<int>(r0[j])) << 16) +
+                            (static_cast<long long>(static_cast<int>(r1[j])) << 8) +
+                            static_cast<long long>(static_cast<int>(r2[j]));
         v[j] = static_cast<float>(fma(static_cast<double>(t), fabs(__ldg(p.rscale + e.m_first + j)), double(e.bf)));
       }
     }
@@ -605,23 +604,9 @@ __device__ __forceinline__ void emit16_limbs(const uint32_t (&r0)[16], const uin
   for (int j = 0; j < 16; ++j)
     v[j] = __fmaf_rn(float(int(r0[j])), sc[j].z,
                      __fmaf_rn(float(int(r1[j])), sc[j].y, __fmaf_rn(float(int(r2[j])), sc[j].x, e.bf)));
-  emit_tail(v, nullptr, r0, r1, r2, e, p, npos, bad);
+  emit_tail(v, r0, r1, r2, e, p, npos, bad);
 }
 
-// from reduced int64 sums (split-K): tot = H 2^24 + L, both exact floats
-__device__ __forceinline__ void emit16_tot(const long long (&tot)[16], const EmitCtx& e, const MmaParams& p,
-                                           unsigned long long& npos, bool& bad) {
-  float4 sc[16];
-  load_scales(e.sc_addr, sc);
-  float v[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int lo = int(uint32_t(tot[j]) & 0xFFFFFFu);
-    const int hi = int(tot[j] >> 24);
-    v[j] = __fmaf_rn(float(hi), sc[j].w, __fmaf_rn(float(lo), sc[j].x, e.bf));
-  }
-  emit_tail(v, tot, nullptr, nullptr, nullptr, e, p, npos, bad);
-}
 
 template <int MT, int CS>
 __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
@@ -927,12 +912,16 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
           emit16_limbs(r0, r1, r2, ctx(mm), p, npos, any_bad);
           if (et == 0 && lu == 0) TG_STAMP(7, 240 + mm / 16);
         } else if (!ghost) {
-          long long* dst = p.part + (int64_t(split) * p.M_pad + m0 + mm) * p.N_pad + n;
+          // per-limb partials: the reduced sums take exactly the unsplit epilogue, so a
+          // row's bits do not depend on whether its GEMM was split
+          const int64_t plane = int64_t(p.M_pad) * p.N_pad;
+          int32_t* dst = p.part + 3 * int64_t(split) * plane + int64_t(m0 + mm) * p.N_pad + n;
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            dst[int64_t(j) * p.N_pad] = (static_cast<long long>(static_cast<int>(r0[j])) << 16) +
-                                        (static_cast<long long>(static_cast<int>(r1[j])) << 8) +
-                                        static_cast<long long>(static_cast<int>(r2[j]));
+          for (int j = 0; j < 16; ++j) {
+            dst[int64_t(j) * p.N_pad] = int32_t(r0[j]);
+            dst[plane + int64_t(j) * p.N_pad] = int32_t(r1[j]);
+            dst[2 * plane + int64_t(j) * p.N_pad] = int32_t(r2[j]);
+          }
         }
       }
       // TMEM buffer can be reused by the MMA warp
@@ -942,7 +931,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
       if (et == 0 && lu == 0) TG_STAMP(7, 120);
 
       if (p.splits > 1 && !ghost) {
-        // last-arriving unit of this (mb, nb) tile reduces the int64 partials
+        // last-arriving unit of this (mb, nb) tile reduces the limb partials
         __threadfence();
         named_bar_sync(1, ET);
         if (et == 0) {
@@ -957,18 +946,28 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
           __threadfence();
 #pragma unroll 1
           for (int j0 = 16 * half; j0 < MT; j0 += 32) {
-            // 16 independent rows per batch so the L2 reads of the partials overlap
-            long long tot[16];
-            const long long* src = p.part + int64_t(m0 + j0) * p.N_pad + n;
+            // 16 independent rows per batch so the L2 reads of the partials overlap;
+            // int32 sums stay exact (|S_l| < 128 K < 2^31)
+            const int64_t plane = int64_t(p.M_pad) * p.N_pad;
+            uint32_t t0[16], t1[16], t2[16];
+            const int32_t* src = p.part + int64_t(m0 + j0) * p.N_pad + n;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) tot[j] = __ldcg(src + int64_t(j) * p.N_pad);
+            for (int j = 0; j < 16; ++j) {
+              t0[j] = uint32_t(__ldcg(src + int64_t(j) * p.N_pad));
+              t1[j] = uint32_t(__ldcg(src + plane + int64_t(j) * p.N_pad));
+              t2[j] = uint32_t(__ldcg(src + 2 * plane + int64_t(j) * p.N_pad));
+            }
 #pragma unroll 1
             for (int sp = 1; sp < p.splits; ++sp) {
-              const long long* s2 = src + int64_t(sp) * p.M_pad * p.N_pad;
+              const int32_t* s2 = src + 3 * int64_t(sp) * plane;
 #pragma unroll
-              for (int j = 0; j < 16; ++j) tot[j] += __ldcg(s2 + int64_t(j) * p.N_pad);
+              for (int j = 0; j < 16; ++j) {
+                t0[j] += uint32_t(__ldcg(s2 + int64_t(j) * p.N_pad));
+                t1[j] += uint32_t(__ldcg(s2 + plane + int64_t(j) * p.N_pad));
+                t2[j] += uint32_t(__ldcg(s2 + 2 * plane + int64_t(j) * p.N_pad));
+              }
             }
-            emit16_tot(tot, ctx(j0), p, npos, any_bad);
+            emit16_limbs(t0, t1, t2, ctx(j0), p, npos, any_bad);
           }
         }
         named_bar_sync(1, ET);  // last_flag is reused by the next unit
@@ -1331,7 +1330,8 @@ static SplitLayout split_layout(int64_t M, int64_t K, int64_t N) {
   L.total_prepare = L.off_rscale + size_t(round_up(L.M_pad * int64_t(sizeof(double)), 256));
   L.off_counters = L.total_prepare;
   L.off_part = L.off_counters + size_t(round_up(L.MB * L.NB * 4, 256));
-  L.total = L.splits > 1 ? L.off_part + size_t(L.splits) * size_t(L.M_pad) * size_t(L.N_pad) * 8 : L.total_prepare;
+  L.total = L.splits > 1 ? L.off_part + size_t(L.splits) * 3 * size_t(L.M_pad) * size_t(L.N_pad) * 4
+                         : L.total_prepare;
   return L;
 }
 
@@ -1497,7 +1497,7 @@ int run_mma(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* t
   }
   if (L.splits > 1) {
     p.counters = reinterpret_cast<int32_t*>(base + L.off_counters);
-    p.part = reinterpret_cast<long long*>(base + L.off_part);
+    p.part = reinterpret_cast<int32_t*>(base + L.off_part);
     cudaError_t e = cudaMemsetAsync(p.counters, 0, size_t(L.MB * L.NB) * 4, st);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaMemsetAsync(split counters)");
   }

@@ -12,6 +12,9 @@ path never synchronises.
 
 from __future__ import annotations
 
+import threading
+import weakref
+
 import numpy as np
 import torch
 
@@ -30,21 +33,59 @@ def _is_tensor(v) -> bool:
     return isinstance(v, torch.Tensor)
 
 
+class _PinnedPool:
+    """Pinned host buffers for results, recycled when the numpy array handed out
+    is garbage-collected.  A fresh pinned allocation costs ~100 us on this box
+    (and can stall the device); a result D2H of a few MB costs less than that."""
+
+    def __init__(self):
+        self._free: dict[tuple, list[torch.Tensor]] = {}
+        self._lock = threading.Lock()
+
+    def take(self, shape: tuple, dtype: torch.dtype) -> torch.Tensor:
+        key = (tuple(int(s) for s in shape), dtype)
+        with self._lock:
+            lst = self._free.get(key)
+            if lst:
+                return lst.pop()
+        return torch.empty(key[0], dtype=dtype, pin_memory=True)
+
+    def give(self, t: torch.Tensor) -> None:
+        with self._lock:
+            lst = self._free.setdefault((tuple(t.shape), t.dtype), [])
+            if len(lst) < 8:
+                lst.append(t)
+
+    def lease(self, t: torch.Tensor) -> np.ndarray:
+        """numpy view of ``t``; ``t`` returns to the pool when the view (and every
+        view of it) is gone."""
+        a = t.numpy()
+        weakref.finalize(a, self.give, t)
+        return a
+
+
+_pinned = _PinnedPool()
+
+
 def _to_host(d: torch.Tensor, extra: torch.Tensor | None = None):
     """Device -> host through pinned memory (one stream-ordered async copy, one
     synchronisation); ``extra`` (a small status tensor) rides along and is
-    returned too.  Pinned blocks come from torch's caching host allocator."""
+    returned too."""
     if not d.is_cuda:
         h = d.numpy()
         return (h, extra.cpu().numpy()) if extra is not None else h
-    h = torch.empty(d.shape, dtype=d.dtype, pin_memory=True)
+    h = _pinned.take(d.shape, d.dtype)
     h.copy_(d, non_blocking=True)
     he = None
     if extra is not None:
-        he = torch.empty(extra.shape, dtype=extra.dtype, pin_memory=True)
+        he = _pinned.take(extra.shape, extra.dtype)
         he.copy_(extra, non_blocking=True)
     torch.cuda.current_stream(d.device).synchronize()
-    return (h.numpy(), he.numpy()) if extra is not None else h.numpy()
+    if extra is None:
+        return _pinned.lease(h)
+    f = he.numpy().copy()
+    _pinned.give(he)
+    return _pinned.lease(h), f
 
 
 class _Dual:
@@ -142,6 +183,8 @@ class DenseMatrix:
     its non-finite bit is turned into the reference's ParameterError the first
     time the host looks at the values (or on ``check()``)."""
 
+    _arrival = None  # streamed result: (pinned host Y, pinned host flags, event of their copies)
+
     def __init__(self, values, _flags: torch.Tensor | None = None):
         self._flags = _flags
         self._checked = _flags is None
@@ -163,7 +206,31 @@ class DenseMatrix:
         self._v = _Dual(v, None)
         self._checked = True
 
+    @classmethod
+    def _streamed(cls, dev: torch.Tensor, host: torch.Tensor, host_flags: torch.Tensor,
+                  done: torch.cuda.Event) -> "DenseMatrix":
+        """A kernel output whose host copy (and status words) are already on their
+        way through pinned memory; ``done`` marks their arrival."""
+        obj = cls(dev, _flags=host_flags)
+        obj._arrival = (host, done)
+        return obj
+
+    def _arrive(self) -> None:
+        host, done = self._arrival
+        done.synchronize()
+        self._arrival = None
+        f = self._flags
+        self._flags = f.clone()
+        _pinned.give(f)
+        if _flags_bad(self._flags.numpy()):
+            _pinned.give(host)
+            raise ParameterError("dense matrix contains non-finite values")
+        self._checked = True
+        self._v._h = _pinned.lease(host)
+
     def check(self) -> "DenseMatrix":
+        if self._arrival is not None:
+            self._arrive()
         if not self._checked:
             if self._flags is not None:
                 bad = _flags_bad(self._flags.cpu().numpy())
@@ -176,6 +243,8 @@ class DenseMatrix:
 
     @property
     def values(self) -> np.ndarray:
+        if self._arrival is not None:
+            self._arrive()
         v = self._v
         if v._h is None and not self._checked and self._flags is not None and v._d is not None and v._d.is_cuda:
             # fetch Y and the kernel's status words with one synchronisation

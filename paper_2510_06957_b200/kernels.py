@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .dense import BiasVector, DenseMatrix, TernaryDense, _Dual, _device, as_bias, as_dense, as_ternary
+from .dense import BiasVector, DenseMatrix, TernaryDense, _Dual, _device, _pinned, as_bias, as_dense, as_ternary
 from .errors import ParameterError
 from .formats import (
     DEFAULT_GROUP_SIMD,
@@ -117,49 +117,76 @@ class PaddedInput:
             raise ParameterError("padded slot (last column) must be exactly zero")
         self._v = _Dual(v, None)
 
+    _pending = None  # pad_input of a host X: the unpadded host tensor, not uploaded yet
+
     @classmethod
     def _trusted(cls, dev: torch.Tensor) -> "PaddedInput":
         obj = cls.__new__(cls)
         obj._v = _Dual(None, dev)
         return obj
 
+    @classmethod
+    def _from_host(cls, src: torch.Tensor) -> "PaddedInput":
+        obj = cls.__new__(cls)
+        obj._v = None
+        obj._pending = src
+        return obj
+
+    def _materialise(self) -> None:
+        src = self._pending
+        M, K = int(src.shape[0]), int(src.shape[1])
+        xp = torch.empty((M, K + 1), dtype=torch.float32, device=_device())
+        xp[:, :-1].copy_(src, non_blocking=src.is_pinned())
+        xp[:, -1].zero_()
+        self._v, self._pending = _Dual(None, xp), None
+
+    @property
+    def _hsrc(self) -> torch.Tensor | None:
+        """Host tensor to stream from ([M, K] pending, or the full padded host array)."""
+        if self._pending is not None:
+            return self._pending
+        return _host_source(self._v)
+
     @property
     def values(self) -> np.ndarray:
+        if self._pending is not None:
+            h = self._pending.numpy()
+            return np.concatenate([h, np.zeros((h.shape[0], 1), np.float32)], axis=1)
         return self._v.host()
 
     @property
     def device_values(self) -> torch.Tensor:
+        if self._pending is not None:
+            self._materialise()
         return self._v.dev()
 
     @property
     def M(self) -> int:
-        return self._v.shape()[0]
+        return int(self._pending.shape[0]) if self._pending is not None else self._v.shape()[0]
 
     @property
     def K(self) -> int:
-        return self._v.shape()[1] - 1
+        return int(self._pending.shape[1]) if self._pending is not None else self._v.shape()[1] - 1
 
     def logical(self) -> DenseMatrix:
         return DenseMatrix(self.device_values[:, :-1].contiguous())
 
 
 def pad_input(X) -> PaddedInput:
-    """simd.py:72-75, on the device.  A host input is copied straight into the
-    padded device buffer (one strided, stream-ordered copy; asynchronous from
-    pinned memory) instead of uploading X and copying it again."""
+    """simd.py:72-75, on the device.  A host input is not copied here: it goes
+    straight into the padded device buffer when first needed -- streamed in
+    row chunks by a GEMM (GemmRunner.run_from_host), or one strided copy on
+    ``device_values`` -- instead of uploading X and copying it again."""
     X = as_dense(X)
     v = X._v
     if v._d is not None and v._d.is_cuda:
         x = v._d
         xp = torch.empty((x.shape[0], x.shape[1] + 1), dtype=torch.float32, device=x.device)
         xp[:, :-1].copy_(x)
-    else:
-        src = v._d if v._d is not None else torch.from_numpy(np.ascontiguousarray(v._h))
-        M, K = int(src.shape[0]), int(src.shape[1])
-        xp = torch.empty((M, K + 1), dtype=torch.float32, device=_device())
-        xp[:, :-1].copy_(src, non_blocking=src.is_pinned())
-    xp[:, -1].zero_()
-    return PaddedInput._trusted(xp)
+        xp[:, -1].zero_()
+        return PaddedInput._trusted(xp)
+    _device()  # no CUDA device: fail here, like the device path
+    return PaddedInput._from_host(_host_source(v))
 
 
 # ---------------------------------------------------------------- device plumbing
@@ -180,6 +207,16 @@ def _workspace(nbytes: int, dev: torch.device, stream: int) -> torch.Tensor:
             t = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
             _ws_cache[key] = t
     return t
+
+
+STREAM_MIN_BYTES = 1 << 20   # host X below this is uploaded whole
+
+
+def _host_source(v) -> torch.Tensor | None:
+    """The host tensor behind an operand that is not on the device yet, else None."""
+    if v._d is not None:
+        return None if v._d.is_cuda else v._d
+    return torch.from_numpy(np.ascontiguousarray(v._h))
 
 
 def _p(t):
@@ -275,15 +312,25 @@ class GemmRunner:
             r.a0, r.a1 = f.device("col_segment_ptr").data_ptr(), f.device("all_indices").data_ptr()
         return r
 
-    def launch(self, stream: int | None = None, ws: torch.Tensor | None = None, stage: str = "all") -> None:
+    def launch(self, stream: int | None = None, ws: torch.Tensor | None = None, stage: str = "all",
+               rows: tuple[int, int] | None = None) -> None:
         """Issue the call.  For the tensor-core path ``stage`` may be "prepare"
         (X limb split) or "run" (tile MMA + exact-order fix-up) so a caller can
-        time the two halves separately; "all" issues both."""
+        time the two halves separately; "all" issues both.  ``rows`` = (r0, r1)
+        restricts the call to those rows of X and Y (every kernel computes rows
+        independently; r0 must be a multiple of ``mr`` for the blocked order)."""
         st = torch.cuda.current_stream().cuda_stream if stream is None else stream
         if ws is None:
             ws = self._ws if self._ws is not None else _workspace(self.ws_bytes, self.x.device, st)
         x, y, b, fl = _p(self.x), _p(self.y), _p(self.bias), _p(self.flags)
         M, K, N, ldx = self.M, self.K, self.N, self.ldx
+        if rows is not None:
+            r0, r1 = rows
+            if self.scatter is not None or not 0 <= r0 < r1 <= self.M or r0 % self.mr:
+                raise ParameterError(f"bad row range {rows} for M = {self.M}, mr = {self.mr}")
+            x = ctypes.c_void_p(self.x.data_ptr() + 4 * r0 * ldx)
+            y = ctypes.c_void_p(self.y.data_ptr() + 4 * r0 * self.ldy)
+            M = r1 - r0
         f = self.fmt
         if self.method == "mma":
             if stage in ("all", "prepare"):
@@ -340,6 +387,34 @@ class GemmRunner:
         torch.cuda.current_stream().wait_stream(s)
         return g
 
+    def run_from_host(self, hx: torch.Tensor) -> DenseMatrix:
+        """X arrives from host memory (tensor-core path): the library streams it
+        in row chunks, each chunk's host->device copy, GEMM and device->host
+        copy of Y on its own stream, so the two PCIe directions and the GEMMs
+        overlap (tg_gemm_tiles_host).  ``hx`` is [M, <= ldx] (pinned for
+        asynchronous copies); columns of x beyond it are zeroed (the padded
+        input's slot).  Returns a DenseMatrix whose host values arrive with the
+        last chunk."""
+        if self.method != "mma" or self.scatter is not None:
+            raise ParameterError("host streaming runs the tensor-core path")
+        hx = hx.contiguous()
+        dev = self.x.device
+        st = torch.cuda.current_stream(dev).cuda_stream
+        L = nat.load()
+        ws_bytes = L.tg_gemm_host_workspace_bytes(self.M, self.K, self.N)
+        ws = _workspace(ws_bytes, dev, st) if self._ws is None or self._ws.numel() < ws_bytes else self._ws
+        y_host = _pinned.take((self.M, self.N), torch.float32)
+        ldx_h = int(hx.shape[1])
+        nat.call("tg_gemm_tiles_host", ctypes.c_void_p(hx.data_ptr()), self.M, self.K, ldx_h, _p(self.x), self.ldx,
+                 _p(self.tiles), self.N, _p(self.bias), _p(self.y), self.ldy, ctypes.c_void_p(y_host.data_ptr()),
+                 self.N, self.use_alpha, self.alpha, ctypes.byref(self.exact), _p(ws), ws.numel(), _p(self.flags),
+                 st)
+        f_host = _pinned.take(self.flags.shape, self.flags.dtype)
+        f_host.copy_(self.flags, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(torch.cuda.current_stream(dev))
+        return DenseMatrix._streamed(self.y, y_host, f_host, done)
+
     def pin_workspace(self) -> None:
         """Give this runner a private workspace (needed for graph capture / concurrent replays)."""
         self._ws = torch.empty(max(self.ws_bytes, 1), dtype=torch.uint8, device=self.x.device)
@@ -352,9 +427,26 @@ class GemmRunner:
         return int(f[2]) | (int(f[3]) << 32)
 
 
-def _finish(runner: GemmRunner, counted: bool, adds: int):
-    runner.launch()
-    y = runner.result()
+def _x_operand(X, method: str) -> tuple[torch.Tensor, torch.Tensor | None]:
+    """Device buffer for X (DenseMatrix or PaddedInput) and, when X is still in
+    host memory and large enough to pay for chunking, the host tensor to stream
+    into it (GemmRunner.run_from_host, tensor-core path); otherwise X uploaded
+    whole and None."""
+    if isinstance(X, PaddedInput):
+        hs, cols = X._hsrc, X.K + 1
+    else:
+        hs, cols = _host_source(X._v), X.cols
+    if method == "mma" and hs is not None and hs.numel() * 4 >= STREAM_MIN_BYTES and hs.shape[0] >= 128:
+        return torch.empty((int(hs.shape[0]), cols), dtype=torch.float32, device=_device()), hs
+    return X.device_values, None
+
+
+def _finish(runner: GemmRunner, counted: bool, adds: int, hx: torch.Tensor | None = None):
+    if hx is not None:
+        y = runner.run_from_host(hx)
+    else:
+        runner.launch()
+        y = runner.result()
     if not counted:
         return y
     mults = runner.nonpositive() if runner.use_alpha else 0
@@ -393,8 +485,9 @@ def gemm_base(X, t, b, counted: bool = False, *, method: str | None = None):
     X, b, t = as_dense(X), as_bias(b), _as_tcsc(t)
     _check_dims(X.cols, t.K, len(b), t.N)
     m = _method(None, method, t.K, t.N, t.nnz)
-    r = GemmRunner("base", X.device_values, t, b.device_values, method=m)
-    return _finish(r, counted, X.rows * t.N + X.rows * t.nnz)
+    xd, hx = _x_operand(X, m)
+    r = GemmRunner("base", xd, t, b.device_values, method=m)
+    return _finish(r, counted, X.rows * t.N + X.rows * t.nnz, hx)
 
 
 def gemm_unrolled(X, t, b, cfg: GemmConfig | None = None, counted: bool = False, *, method: str | None = None):
@@ -403,9 +496,10 @@ def gemm_unrolled(X, t, b, cfg: GemmConfig | None = None, counted: bool = False,
     X, b, t = as_dense(X), as_bias(b), _as_tcsc(t)
     _check_dims(X.cols, t.K, len(b), t.N)
     m = _method(cfg, method, t.K, t.N, t.nnz)
-    r = GemmRunner("unrolled", X.device_values, t, b.device_values, method=m, uf=cfg.uf)
+    xd, hx = _x_operand(X, m)
+    r = GemmRunner("unrolled", xd, t, b.device_values, method=m, uf=cfg.uf)
     M = X.rows
-    return _finish(r, counted, M * t.nnz + M * t.N * (cfg.uf + 1))
+    return _finish(r, counted, M * t.nnz + M * t.N * (cfg.uf + 1), hx)
 
 
 def gemm_blocked(X, t, b, cfg: GemmConfig | None = None, counted: bool = False, *, method: str | None = None):
@@ -414,10 +508,11 @@ def gemm_blocked(X, t, b, cfg: GemmConfig | None = None, counted: bool = False, 
     X, b, t = as_dense(X), as_bias(b), _as_blocked(t)
     _check_dims(X.cols, t.K, len(b), t.N)
     m = _method(cfg, method, t.K, t.N, t.nnz)
-    r = GemmRunner("blocked", X.device_values, t, b.device_values, method=m, uf=cfg.uf, mr=cfg.mr)
+    xd, hx = _x_operand(X, m)
+    r = GemmRunner("blocked", xd, t, b.device_values, method=m, uf=cfg.uf, mr=cfg.mr)
     M, nb = X.rows, t.num_blocks
     mf = M // cfg.mr * cfg.mr
-    return _finish(r, counted, M * t.nnz + mf * t.N * nb * (cfg.uf + 1) + (M - mf) * t.N * nb)
+    return _finish(r, counted, M * t.nnz + mf * t.N * nb * (cfg.uf + 1) + (M - mf) * t.N * nb, hx)
 
 
 def gemm_interleaved_blocked(X, t, b, cfg: GemmConfig | None = None, counted: bool = False, *,
@@ -431,9 +526,10 @@ def gemm_interleaved_blocked(X, t, b, cfg: GemmConfig | None = None, counted: bo
             "scalar kernel cannot consume symmetric-group formats (dummy index needs a padded input row)"
         )
     m = _method(cfg, method, t.K, t.N, t.nnz)
-    r = GemmRunner("interleaved_blocked", X.device_values, t, b.device_values, method=m)
+    xd, hx = _x_operand(X, m)
+    r = GemmRunner("interleaved_blocked", xd, t, b.device_values, method=m)
     M = X.rows
-    return _finish(r, counted, M * t.nnz + M * t.N * t.num_blocks)
+    return _finish(r, counted, M * t.nnz + M * t.N * t.num_blocks, hx)
 
 
 def gemm_vectorized_optimal(Xp, t, b, alpha: float | None = None, cfg: GemmConfig | None = None,
@@ -450,8 +546,9 @@ def gemm_vectorized_optimal(Xp, t, b, alpha: float | None = None, cfg: GemmConfi
     _alpha_args(alpha)
     n_idx = t._len("all_indices")
     m = _method(cfg, method, t.K, t.N, n_idx)
-    r = GemmRunner("vectorized_optimal", Xp.device_values, t, b.device_values, method=m, alpha=alpha)
-    return _finish(r, counted, Xp.M * (n_idx + t.N * t.num_blocks))
+    xd, hx = _x_operand(Xp, m)
+    r = GemmRunner("vectorized_optimal", xd, t, b.device_values, method=m, alpha=alpha)
+    return _finish(r, counted, Xp.M * (n_idx + t.N * t.num_blocks), hx)
 
 
 def _as_sym(t) -> SymmetricInterleavedTcsc:
@@ -474,9 +571,10 @@ def _symmetric_kernel(kind: str, Xp, t, b, alpha, counted, method):
     _alpha_args(alpha)
     n_idx = t._len("indices")
     m = _method(None, method, t.K, t.N, n_idx)
-    r = GemmRunner(kind, Xp.device_values, t, b.device_values, method=m, alpha=alpha)
+    xd, hx = _x_operand(Xp, m)
+    r = GemmRunner(kind, xd, t, b.device_values, method=m, alpha=alpha)
     extra = 2 if kind == "vertical" else 4  # simd.py:167-170 (b + p - q) / :253-256 (pairwise + b)
-    return _finish(r, counted, Xp.M * (n_idx + extra * t.N))
+    return _finish(r, counted, Xp.M * (n_idx + extra * t.N), hx)
 
 
 def gemm_vertical(Xp, t, b, alpha: float | None = None, counted: bool = False, *, method: str | None = None):
@@ -500,9 +598,10 @@ def gemm_compressed(X, t, b, counted: bool = False, *, method: str | None = None
     if m == "auto":
         m = "mma" if t.K <= (1 << 24) else "gather"  # the code stream is dense: density gives no signal
     m = choose_method(m, t.K, t.N, t.K * t.N)
-    r = GemmRunner("compressed", X.device_values, t, b.device_values, method=m)
+    xd, hx = _x_operand(X, m)
+    r = GemmRunner("compressed", xd, t, b.device_values, method=m)
     nnz = t.nnz if counted else 0
-    return _finish(r, counted, X.rows * nnz + X.rows * t.N)
+    return _finish(r, counted, X.rows * nnz + X.rows * t.N, hx)
 
 
 # ---------------------------------------------------------------- registry (kernels/__init__.py:66-230)

@@ -132,3 +132,39 @@ def test_nonfinite_input_is_reported(tg):
     t = tg.tcsc_from_dense(tg.TernaryDense(W))
     with pytest.raises(ParameterError):
         tg.gemm_base(X, t, torch.zeros(N, device="cuda"), method="mma").values
+
+
+@pytest.mark.parametrize("method", ["mma", "gather"])
+def test_host_input_is_streamed_bit_exact(tg, method):
+    """Host X (pinned tensor, numpy) goes through the row-chunked H2D / GEMM / D2H
+    pipeline; every entry point must give the bits of the device-resident call."""
+    from paper_2510_06957_b200 import _native as nat
+
+    M, K, N = 700, 1024, 320   # 2.9 MB of X: several chunks, a ragged last one
+    rng = np.random.default_rng(3)
+    W = rng.integers(-1, 2, size=(K, N)).astype(np.int8)
+    X = rng.standard_normal((M, K)).astype(np.float32)
+    X[5, 3] = 4e4  # a wide row in the middle of a chunk
+    b = rng.standard_normal(N).astype(np.float32)
+    assert nat.load().tg_gemm_host_workspace_bytes(M, K + 1, N) > nat.load().tg_gemm_workspace_bytes(192, K + 1, N)
+    Wd = torch.from_numpy(W).cuda()
+    Xd = torch.from_numpy(X).cuda()
+    Xpin = torch.from_numpy(X).pin_memory()
+    cfg = tg.GemmConfig(uf=2, mr=2, alpha=0.25)
+    t = tg.tcsc_from_dense(tg.TernaryDense(Wd))
+    bl = tg.blocked_from_dense(tg.TernaryDense(Wd), 256)
+    ib = tg.interleaved_blocked_from_dense(Wd, 256, 2, False)
+    ibs = tg.interleaved_blocked_from_dense(Wd, 256, 2, True)
+    calls = [
+        lambda x: tg.gemm_base(x, t, b, method=method),
+        lambda x: tg.gemm_unrolled(x, t, b, cfg, method=method),
+        lambda x: tg.gemm_blocked(x, bl, b, cfg, method=method),
+        lambda x: tg.gemm_interleaved_blocked(x, ib, b, method=method),
+        lambda x: tg.gemm_vectorized_optimal(tg.pad_input(x), ibs, b, 0.25, method=method),
+    ]
+    for i, call in enumerate(calls):
+        ref = call(Xd).values
+        for x in (Xpin, X):
+            y = call(x)
+            assert np.array_equal(y.values, ref), (i, type(x))
+            assert torch.equal(y.device_values.cpu(), torch.from_numpy(ref))
