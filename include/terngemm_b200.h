@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define TG_ABI_VERSION 3
+#define TG_ABI_VERSION 4
 
 typedef enum {
   TG_OK = 0,
@@ -227,7 +227,7 @@ int tg_gemm_tiles(const float* X, int64_t M, int64_t K, int64_t ldx, const uint3
                   void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream);
 
 /* Host-resident X and Y: the reference's own calling convention (numpy in,
- * numpy out, dense.py:67-90).  X rows are streamed in chunks of about 2 MB;
+ * numpy out, dense.py:67-90).  X rows are streamed in chunks of about 512 KB;
  * each chunk's host->device copy (2-D, into the device staging X_dev of row
  * pitch ldx_dev, whose columns K..ldx_dev-1 are zeroed: the padded input's
  * slot, simd.py:72-75), X split + tile GEMM, and device->host copy of its Y
@@ -236,12 +236,20 @@ int tg_gemm_tiles(const float* X, int64_t M, int64_t K, int64_t ldx, const uint3
  * respect to `stream` (forks from it and joins back).  Host buffers should be
  * pinned for the copies to be asynchronous.  Rows are independent and the
  * epilogue does not depend on the chunking: Y is bit-identical to
- * tg_gemm_tiles on the whole X.                                               */
+ * tg_gemm_tiles on the whole X.
+ * With flags_host != NULL the call owns the status words: it zeroes `flags`
+ * first and copies them to flags_host (pinned) after the last chunk, so one
+ * synchronisation of `stream` delivers Y and its status together.
+ * A call whose arguments (every pointer and size) repeat an earlier call's is
+ * replayed from a CUDA graph of that call: one launch instead of ~25 API calls
+ * (TG_HOST_GRAPHS=0 disables it; a caller that is capturing `stream` itself
+ * gets the plain enqueue).                                                     */
 size_t tg_gemm_host_workspace_bytes(int64_t M, int64_t K, int64_t N);
 int tg_gemm_tiles_host(const float* X_host, int64_t M, int64_t K, int64_t ldx_host, float* X_dev, int64_t ldx_dev,
                        const uint32_t* tiles, int64_t N, const float* bias, float* Y_dev, int64_t ldy_dev,
                        float* Y_host, int64_t ldy_host, int use_alpha, float alpha, const tg_format_ref* exact,
-                       void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream);
+                       void* ws, size_t ws_bytes, tg_device_flags* flags, tg_device_flags* flags_host,
+                       void* stream);
 
 /* ---------------------------------------------------------------- peer scatter
  * Column-sharded GEMM whose epilogue writes every finished Y tile straight

@@ -150,7 +150,7 @@ SIGNATURES: dict[str, tuple] = {
     "tg_gemm_host_workspace_bytes": (_SZ, [_I64, _I64, _I64]),
     "tg_gemm_tiles_host": (
         _I,
-        [_P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _P, _I64, _P, _I64, _I, _F, _P, _P, _SZ, _P, _P],
+        [_P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _P, _I64, _P, _I64, _I, _F, _P, _P, _SZ, _P, _P, _P],
     ),
     "tg_peer_alloc": (_I, [_SZ, ctypes.POINTER(_P)]),
     "tg_peer_free": (_I, [_P]),

@@ -302,10 +302,10 @@ int tg_gemm_tiles(const float* X, int64_t M, int64_t K, int64_t ldx, const uint3
 // ------------------------------------------------------------------ GEMM from host memory
 namespace {
 
-// Row chunks of a host-resident X: about 2 MB of X each (a chunk's PCIe time,
-// ~40 us, must cover the ~25 us of host work to enqueue the next one), at most
-// 8, starting at multiples of 64 rows (a multiple of every blocked-order row
-// unroll mr).
+// Row chunks of a host-resident X: about 512 KB of X each, at most 8, starting
+// at multiples of 64 rows (a multiple of every blocked-order row unroll mr).
+// Small chunks let the two PCIe directions and the GEMMs overlap; what they
+// cost in host work is paid once, when the call is captured in a graph.
 struct HostPlan {
   int64_t rows, n;  // chunk height (the last one may be shorter), chunk count
   int streams;      // side streams used
@@ -317,7 +317,7 @@ HostPlan host_plan(int64_t M, int64_t K, int64_t N) {
   const int64_t bytes = M * K * 4;
   int64_t cap = 8;
   if (const char* env = getenv("TG_HOST_CHUNKS")) cap = std::max(1, atoi(env));
-  int64_t n = std::max<int64_t>(1, std::min<int64_t>({cap, bytes >> 21, M / 64}));
+  int64_t n = std::max<int64_t>(1, std::min<int64_t>({cap, bytes >> 19, M / 64}));
   P.rows = round_up(ceil_div(M, n), 64);
   P.n = ceil_div(M, P.rows);
   P.streams = int(std::min<int64_t>(P.n, 4));
@@ -326,11 +326,13 @@ HostPlan host_plan(int64_t M, int64_t K, int64_t N) {
   return P;
 }
 
-// The library's own side streams and events, per device (created once).
+// The library's own side streams and events, per device (created once), and
+// the stream host-streaming calls are captured on.
 struct SideStreams {
   cudaStream_t s[4];
   cudaEvent_t join[4];
   cudaEvent_t fork;
+  cudaStream_t capture;
 };
 
 int side_streams(SideStreams** out) {
@@ -348,12 +350,111 @@ int side_streams(SideStreams** out) {
           (e = cudaEventCreateWithFlags(&ss.join[i], cudaEventDisableTiming)) != cudaSuccess)
         return set_cuda_error(e, "side stream creation");
     }
-    if ((e = cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming)) != cudaSuccess)
+    if ((e = cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&ss.capture, cudaStreamNonBlocking)) != cudaSuccess)
       return set_cuda_error(e, "side stream creation");
     it = per_dev.emplace(dev, ss).first;
   }
   *out = &it->second;
   return TG_OK;
+}
+
+// Every argument of one host-streaming call, plus the device and the chunk
+// plan: two calls with equal keys enqueue exactly the same work, so the second
+// one onwards can replay a CUDA graph of the first instead of issuing ~25 API
+// calls (the graph launch is one).  Compared bytewise: zero-initialised.
+struct HostKey {
+  const float* X_host;
+  int64_t M, K, ldx_host;
+  float* X_dev;
+  int64_t ldx_dev;
+  const uint32_t* tiles;
+  int64_t N;
+  const float* bias;
+  float* Y_dev;
+  int64_t ldy_dev;
+  float* Y_host;
+  int64_t ldy_host;
+  int32_t use_alpha;
+  float alpha;
+  int32_t has_exact, dev;
+  tg_format_ref exact;
+  void* ws;
+  size_t ws_bytes;
+  tg_device_flags* flags;
+  tg_device_flags* flags_host;
+  int64_t rows, n;
+};
+
+struct HostGraph {
+  HostKey key;
+  cudaGraphExec_t exec;  // null until the key has been seen twice
+  bool tried;            // capture attempted (a failed capture is not retried)
+  uint64_t last_use;
+};
+
+constexpr int kHostGraphs = 16;
+
+int enqueue_host(const HostKey& k, const HostPlan& P, SideStreams* ss, cudaStream_t main) {
+  cudaError_t e;
+  if (k.flags_host && (e = cudaMemsetAsync(k.flags, 0, sizeof(tg_device_flags), main)) != cudaSuccess)
+    return set_cuda_error(e, "cudaMemsetAsync(flags)");
+  if (k.ldx_dev > k.K) {  // the padded input's slot column(s): zero, as pad_input does
+    e = cudaMemset2DAsync(k.X_dev + k.K, size_t(k.ldx_dev) * 4, 0, size_t(k.ldx_dev - k.K) * 4, size_t(k.M), main);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaMemset2DAsync(padded slot)");
+  }
+  if ((e = cudaEventRecord(ss->fork, main)) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
+  for (int i = 0; i < P.streams; ++i)
+    if ((e = cudaStreamWaitEvent(ss->s[i], ss->fork, 0)) != cudaSuccess) return set_cuda_error(e, "fork");
+  const tg_format_ref* exact = k.has_exact ? &k.exact : nullptr;
+  const int64_t M = k.M, K = k.K, N = k.N;
+  for (int64_t c = 0; c < P.n; ++c) {
+    const int i = int(c % P.streams);
+    cudaStream_t st = ss->s[i];
+    const int64_t r0 = c * P.rows, rows = std::min(P.rows, M - r0);
+    float* xd = k.X_dev + r0 * k.ldx_dev;
+    float* yd = k.Y_dev + r0 * k.ldy_dev;
+    void* wsi = static_cast<uint8_t*>(k.ws) + size_t(i) * P.ws_slice;
+    e = k.ldx_dev == K && k.ldx_host == K
+            ? cudaMemcpyAsync(xd, k.X_host + r0 * K, size_t(rows * K) * 4, cudaMemcpyHostToDevice, st)
+            : cudaMemcpy2DAsync(xd, size_t(k.ldx_dev) * 4, k.X_host + r0 * k.ldx_host, size_t(k.ldx_host) * 4,
+                                size_t(K) * 4, size_t(rows), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaMemcpy2DAsync(X chunk)");
+    TG_TRY(tg_gemm_tiles_prepare(xd, rows, K, k.ldx_dev, wsi, P.ws_slice, k.flags, st));
+    TG_TRY(gemm_tiles_run(xd, rows, K, k.ldx_dev, k.tiles, N, k.bias, yd, k.ldy_dev, k.use_alpha, k.alpha, exact,
+                          nullptr, wsi, P.ws_slice, k.flags, st));
+    e = k.ldy_dev == N && k.ldy_host == N
+            ? cudaMemcpyAsync(k.Y_host + r0 * N, yd, size_t(rows * N) * 4, cudaMemcpyDeviceToHost, st)
+            : cudaMemcpy2DAsync(k.Y_host + r0 * k.ldy_host, size_t(k.ldy_host) * 4, yd, size_t(k.ldy_dev) * 4,
+                                size_t(N) * 4, size_t(rows), cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaMemcpy2DAsync(Y chunk)");
+  }
+  for (int i = 0; i < P.streams; ++i) {
+    if ((e = cudaEventRecord(ss->join[i], ss->s[i])) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
+    if ((e = cudaStreamWaitEvent(main, ss->join[i], 0)) != cudaSuccess) return set_cuda_error(e, "join");
+  }
+  if (k.flags_host &&
+      (e = cudaMemcpyAsync(k.flags_host, k.flags, sizeof(tg_device_flags), cudaMemcpyDeviceToHost, main)) !=
+          cudaSuccess)
+    return set_cuda_error(e, "cudaMemcpyAsync(flags)");
+  return TG_OK;
+}
+
+// Capture `k` on the library's capture stream; null on any failure (the caller
+// then enqueues directly, so a graph problem never changes a result).
+cudaGraphExec_t capture_host(const HostKey& k, const HostPlan& P, SideStreams* ss) {
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  if (cudaStreamBeginCapture(ss->capture, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  const int rc = enqueue_host(k, P, ss, ss->capture);
+  const cudaError_t e = cudaStreamEndCapture(ss->capture, &g);
+  if (rc == TG_OK && e == cudaSuccess && g && cudaGraphInstantiate(&exec, g, 0) != cudaSuccess) exec = nullptr;
+  if (g) cudaGraphDestroy(g);
+  cudaGetLastError();
+  return exec;
 }
 
 }  // namespace
@@ -369,9 +470,11 @@ size_t tg_gemm_host_workspace_bytes(int64_t M, int64_t K, int64_t N) {
 int tg_gemm_tiles_host(const float* X_host, int64_t M, int64_t K, int64_t ldx_host, float* X_dev, int64_t ldx_dev,
                        const uint32_t* tiles, int64_t N, const float* bias, float* Y_dev, int64_t ldy_dev,
                        float* Y_host, int64_t ldy_host, int use_alpha, float alpha, const tg_format_ref* exact,
-                       void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream) {
+                       void* ws, size_t ws_bytes, tg_device_flags* flags, tg_device_flags* flags_host,
+                       void* stream) {
   TG_REQUIRE(M >= 1 && K >= 1 && N >= 1, TG_ERR_PARAM, "M, K and N must be >= 1");
   TG_REQUIRE(X_host && X_dev && Y_dev && Y_host && tiles && ws, TG_ERR_PARAM, "null pointer");
+  TG_REQUIRE(!flags_host || flags, TG_ERR_PARAM, "flags_host needs device flags");
   TG_REQUIRE(ldx_host >= K && ldx_dev >= K && ldy_dev >= N && ldy_host >= N, TG_ERR_PARAM,
              "leading dimensions too small");
   TG_REQUIRE(ws_bytes >= tg_gemm_host_workspace_bytes(M, K, N), TG_ERR_PARAM, "workspace too small");
@@ -379,42 +482,55 @@ int tg_gemm_tiles_host(const float* X_host, int64_t M, int64_t K, int64_t ldx_ho
   const HostPlan P = host_plan(M, K, N);
   SideStreams* ss = nullptr;
   TG_TRY(side_streams(&ss));
-  static std::mutex enqueue_mu;  // the side streams and their events are shared by every caller
+  HostKey k;
+  std::memset(&k, 0, sizeof k);
+  k.X_host = X_host, k.M = M, k.K = K, k.ldx_host = ldx_host, k.X_dev = X_dev, k.ldx_dev = ldx_dev;
+  k.tiles = tiles, k.N = N, k.bias = bias, k.Y_dev = Y_dev, k.ldy_dev = ldy_dev, k.Y_host = Y_host;
+  k.ldy_host = ldy_host, k.use_alpha = use_alpha, k.alpha = use_alpha ? alpha : 0.f;
+  k.has_exact = exact != nullptr;
+  if (exact) k.exact = *exact;
+  cudaGetDevice(&k.dev);
+  k.ws = ws, k.ws_bytes = ws_bytes, k.flags = flags, k.flags_host = flags_host, k.rows = P.rows, k.n = P.n;
+
+  static std::mutex enqueue_mu;  // the side streams, their events and the graph table are shared
+  static HostGraph table[kHostGraphs];
+  static int used = 0;
+  static uint64_t clock = 0;
+  static const bool graphs = [] {
+    const char* env = getenv("TG_HOST_GRAPHS");
+    return !(env && env[0] == '0');
+  }();
   std::lock_guard<std::mutex> lk(enqueue_mu);
   cudaStream_t main = as_stream(stream);
-  cudaError_t e;
-  if (ldx_dev > K) {  // the padded input's slot column(s): zero, as pad_input does
-    e = cudaMemset2DAsync(X_dev + K, size_t(ldx_dev) * 4, 0, size_t(ldx_dev - K) * 4, size_t(M), main);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaMemset2DAsync(padded slot)");
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (!graphs || cudaStreamIsCapturing(main, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return enqueue_host(k, P, ss, main);  // the caller is capturing (or graphs are off): plain enqueue
   }
-  if ((e = cudaEventRecord(ss->fork, main)) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
-  for (int i = 0; i < P.streams; ++i)
-    if ((e = cudaStreamWaitEvent(ss->s[i], ss->fork, 0)) != cudaSuccess) return set_cuda_error(e, "fork");
-  for (int64_t c = 0; c < P.n; ++c) {
-    const int i = int(c % P.streams);
-    cudaStream_t st = ss->s[i];
-    const int64_t r0 = c * P.rows, rows = std::min(P.rows, M - r0);
-    float* xd = X_dev + r0 * ldx_dev;
-    float* yd = Y_dev + r0 * ldy_dev;
-    void* wsi = static_cast<uint8_t*>(ws) + size_t(i) * P.ws_slice;
-    e = ldx_dev == K && ldx_host == K
-            ? cudaMemcpyAsync(xd, X_host + r0 * K, size_t(rows * K) * 4, cudaMemcpyHostToDevice, st)
-            : cudaMemcpy2DAsync(xd, size_t(ldx_dev) * 4, X_host + r0 * ldx_host, size_t(ldx_host) * 4,
-                                size_t(K) * 4, size_t(rows), cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaMemcpy2DAsync(X chunk)");
-    TG_TRY(tg_gemm_tiles_prepare(xd, rows, K, ldx_dev, wsi, P.ws_slice, flags, st));
-    TG_TRY(gemm_tiles_run(xd, rows, K, ldx_dev, tiles, N, bias, yd, ldy_dev, use_alpha, alpha, exact, nullptr, wsi,
-                          P.ws_slice, flags, st));
-    e = ldy_dev == N && ldy_host == N
-            ? cudaMemcpyAsync(Y_host + r0 * N, yd, size_t(rows * N) * 4, cudaMemcpyDeviceToHost, st)
-            : cudaMemcpy2DAsync(Y_host + r0 * ldy_host, size_t(ldy_host) * 4, yd, size_t(ldy_dev) * 4,
-                                size_t(N) * 4, size_t(rows), cudaMemcpyDeviceToHost, st);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaMemcpy2DAsync(Y chunk)");
+  // first sighting: enqueue directly and remember the key; second: capture; then replay
+  HostGraph* slot = nullptr;
+  for (int i = 0; i < used; ++i)
+    if (std::memcmp(&table[i].key, &k, sizeof k) == 0) slot = &table[i];
+  if (slot == nullptr) {
+    if (used < kHostGraphs) {
+      slot = &table[used++];
+    } else {
+      slot = &table[0];
+      for (int i = 1; i < used; ++i)
+        if (table[i].last_use < slot->last_use) slot = &table[i];
+      if (slot->exec) cudaGraphExecDestroy(slot->exec);  // an in-flight launch completes first
+    }
+    slot->key = k;
+    slot->exec = nullptr;
+    slot->tried = false;
+    slot->last_use = ++clock;
+    return enqueue_host(k, P, ss, main);
   }
-  for (int i = 0; i < P.streams; ++i) {
-    if ((e = cudaEventRecord(ss->join[i], ss->s[i])) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
-    if ((e = cudaStreamWaitEvent(main, ss->join[i], 0)) != cudaSuccess) return set_cuda_error(e, "join");
-  }
+  slot->last_use = ++clock;
+  if (!slot->tried) slot->exec = capture_host(k, P, ss), slot->tried = true;
+  if (slot->exec == nullptr) return enqueue_host(k, P, ss, main);
+  const cudaError_t e = cudaGraphLaunch(slot->exec, main);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaGraphLaunch(host streaming)");
   return TG_OK;
 }
 

@@ -89,15 +89,23 @@ constexpr float kWideRatio = 16.f;
 constexpr int kMaxScaleExp = 100;
 constexpr int64_t XS_SMEM_MAX_K = 16384;  // rows up to 64 KB are staged in shared memory
 
+// max that propagates NaN (fmaxf drops it), so a NaN anywhere in a row makes
+// its amax non-finite and the row is reported like an inf (dense.py:77).
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
 template <int XS_THREADS>
 __device__ __forceinline__ float block_max(float v, float* red) {
-  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  for (int o = 16; o; o >>= 1) v = fmax_nan(v, __shfl_xor_sync(0xffffffffu, v, o));
   __syncthreads();
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
   __syncthreads();
   v = red[0];
 #pragma unroll
-  for (int i = 1; i < XS_THREADS / 32; ++i) v = fmaxf(v, red[i]);
+  for (int i = 1; i < XS_THREADS / 32; ++i) v = fmax_nan(v, red[i]);
   return v;
 }
 template <int XS_THREADS>
@@ -146,22 +154,22 @@ __global__ void __launch_bounds__(XS_THREADS) tg_xsplit_kernel(const float* __re
         for (int64_t i = threadIdx.x; i < K4; i += XS_THREADS) {
           const float4 v = __ldg(reinterpret_cast<const float4*>(grow) + i);
           reinterpret_cast<float4*>(srow)[i] = v;
-          amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+          amax = fmax_nan(amax, fmax_nan(fmax_nan(fabsf(v.x), fabsf(v.y)), fmax_nan(fabsf(v.z), fabsf(v.w))));
         }
         for (int64_t k = (K4 << 2) + threadIdx.x; k < K; k += XS_THREADS) {
           const float v = __ldg(grow + k);
           srow[k] = v;
-          amax = fmaxf(amax, fabsf(v));
+          amax = fmax_nan(amax, fabsf(v));
         }
       } else {
         for (int64_t k = threadIdx.x; k < K; k += XS_THREADS) {
           const float v = __ldg(grow + k);
           srow[k] = v;
-          amax = fmaxf(amax, fabsf(v));
+          amax = fmax_nan(amax, fabsf(v));
         }
       }
     } else {
-      for (int64_t k = threadIdx.x; k < K; k += XS_THREADS) amax = fmaxf(amax, fabsf(__ldg(grow + k)));
+      for (int64_t k = threadIdx.x; k < K; k += XS_THREADS) amax = fmax_nan(amax, fabsf(__ldg(grow + k)));
     }
   }
   amax = block_max<XS_THREADS>(amax, red);  // (also orders the smem stores before pass 2)
@@ -265,12 +273,12 @@ __global__ void __launch_bounds__(THREADS) tg_xsplit_reg_kernel(const float* __r
   int nz = 0;
 #pragma unroll
   for (int j = 0; j < EPT; ++j) {
-    amax = fmaxf(amax, fabsf(x[j]));
+    amax = fmax_nan(amax, fabsf(x[j]));
     s2 = fma(double(x[j]), double(x[j]), s2);
     nz += x[j] != 0.f;
   }
   for (int o = 16; o; o >>= 1) {
-    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    amax = fmax_nan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     s2 += __shfl_xor_sync(0xffffffffu, s2, o);
     nz += __shfl_xor_sync(0xffffffffu, nz, o);
   }
@@ -286,7 +294,7 @@ __global__ void __launch_bounds__(THREADS) tg_xsplit_reg_kernel(const float* __r
   nz = red_i[0];
 #pragma unroll
   for (int i = 1; i < NW; ++i) {
-    amax = fmaxf(amax, red_f[i]);
+    amax = fmax_nan(amax, red_f[i]);
     s2 += red_d[i];
     nz += red_i[i];
   }
@@ -519,7 +527,7 @@ __device__ __forceinline__ void emit_tail(float (&v)[16], const uint32_t* r0, co
         const bool neg = !(v[j] > 0.f);
         cnt += neg;
         v[j] = neg ? alpha * v[j] : v[j];
-        mx = fmaxf(mx, fabsf(v[j]));
+        mx = fmax_nan(mx, fabsf(v[j]));
       }
       if (e.n_ok) npos += cnt;
     } else {
@@ -529,14 +537,14 @@ __device__ __forceinline__ void emit_tail(float (&v)[16], const uint32_t* r0, co
         const bool neg = !(v[j] > 0.f);
         negbits |= uint32_t(neg) << j;
         v[j] = neg ? alpha * v[j] : v[j];
-        mx = fmaxf(mx, fabsf(v[j]));
+        mx = fmax_nan(mx, fabsf(v[j]));
       }
       const uint32_t live = e.nlive > 0 ? (e.nlive >= 16 ? 0xFFFFu : (1u << e.nlive) - 1u) : 0u;
       if (e.n_ok) npos += __popc(negbits & live & ~(fix ? e.wide_bits : 0u));
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) mx = fmaxf(mx, fabsf(v[j]));  // padded rows / columns are exactly b or 0
+    for (int j = 0; j < 16; ++j) mx = fmax_nan(mx, fabsf(v[j]));  // padded rows / columns are exactly b or 0
   }
   if (!e.n_ok) return;
   bad |= !(mx <= 3.402823466e38f);

@@ -228,6 +228,12 @@ class DenseMatrix:
         self._checked = True
         self._v._h = _pinned.lease(host)
 
+    def _nonpositive(self) -> int:
+        """#(y <= 0) before PReLU from the streamed status words (simd.py:410-417 mults)."""
+        self.check()
+        f = np.asarray(self._flags.numpy() if _is_tensor(self._flags) else self._flags).view(np.uint32)
+        return int(f[2]) | (int(f[3]) << 32)
+
     def check(self) -> "DenseMatrix":
         if self._arrival is not None:
             self._arrive()

@@ -276,10 +276,13 @@ class GemmRunner:
         self.use_alpha, self.alpha = _alpha_args(alpha)
         self.method = method
         dev = x.device
-        self.y = out if out is not None else torch.empty((self.M, self.N), dtype=torch.float32, device=dev)
-        if tuple(self.y.shape) != (self.M, self.N) or self.y.dtype != torch.float32 or self.y.stride(1) != 1:
-            raise ParameterError(f"out must be a float32 [{self.M}, {self.N}] view with unit column stride")
-        self.ldy = int(self.y.stride(0))  # a column block of a wider Y (peer scatter) has ldy > N
+        if out is False:  # a host-streaming plan: every call brings its own Y (run_from_host)
+            self.y, self.ldy = None, self.N
+        else:
+            self.y = out if out is not None else torch.empty((self.M, self.N), dtype=torch.float32, device=dev)
+            if tuple(self.y.shape) != (self.M, self.N) or self.y.dtype != torch.float32 or self.y.stride(1) != 1:
+                raise ParameterError(f"out must be a float32 [{self.M}, {self.N}] view with unit column stride")
+            self.ldy = int(self.y.stride(0))  # a column block of a wider Y (peer scatter) has ldy > N
         self.scatter = scatter
         if scatter is not None and method != "mma":
             raise ParameterError("the peer scatter is fused into the tensor-core epilogue: method must be 'mma'")
@@ -387,33 +390,38 @@ class GemmRunner:
         torch.cuda.current_stream().wait_stream(s)
         return g
 
-    def run_from_host(self, hx: torch.Tensor) -> DenseMatrix:
+    def run_from_host(self, hx: torch.Tensor, bias: torch.Tensor | None = None) -> DenseMatrix:
         """X arrives from host memory (tensor-core path): the library streams it
         in row chunks, each chunk's host->device copy, GEMM and device->host
         copy of Y on its own stream, so the two PCIe directions and the GEMMs
         overlap (tg_gemm_tiles_host).  ``hx`` is [M, <= ldx] (pinned for
         asynchronous copies); columns of x beyond it are zeroed (the padded
-        input's slot).  Returns a DenseMatrix whose host values arrive with the
-        last chunk."""
+        input's slot).  ``bias`` overrides the runner's.  Y is fresh per call
+        (returned to the caller); x, the workspace and the status words are the
+        runner's, so a repeated call repeats every pointer and the library
+        replays its CUDA graph of the first.  Returns a DenseMatrix whose host
+        values and status words arrive together with the last chunk."""
         if self.method != "mma" or self.scatter is not None:
             raise ParameterError("host streaming runs the tensor-core path")
-        hx = hx.contiguous()
+        if not hx.is_contiguous():
+            hx = hx.contiguous()
         dev = self.x.device
-        st = torch.cuda.current_stream(dev).cuda_stream
-        L = nat.load()
-        ws_bytes = L.tg_gemm_host_workspace_bytes(self.M, self.K, self.N)
-        ws = _workspace(ws_bytes, dev, st) if self._ws is None or self._ws.numel() < ws_bytes else self._ws
+        st = torch.cuda.current_stream(dev)
+        ws_bytes = nat.load().tg_gemm_host_workspace_bytes(self.M, self.K, self.N)  # (TG_HOST_CHUNKS may change)
+        if self._ws is None or self._ws.numel() < ws_bytes:
+            self._ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+        ws = self._ws
+        b = self.bias if bias is None else bias
+        y = torch.empty((self.M, self.N), dtype=torch.float32, device=dev)
         y_host = _pinned.take((self.M, self.N), torch.float32)
-        ldx_h = int(hx.shape[1])
-        nat.call("tg_gemm_tiles_host", ctypes.c_void_p(hx.data_ptr()), self.M, self.K, ldx_h, _p(self.x), self.ldx,
-                 _p(self.tiles), self.N, _p(self.bias), _p(self.y), self.ldy, ctypes.c_void_p(y_host.data_ptr()),
-                 self.N, self.use_alpha, self.alpha, ctypes.byref(self.exact), _p(ws), ws.numel(), _p(self.flags),
-                 st)
-        f_host = _pinned.take(self.flags.shape, self.flags.dtype)
-        f_host.copy_(self.flags, non_blocking=True)
+        f_host = _pinned.take((6,), torch.int32)
+        nat.call("tg_gemm_tiles_host", ctypes.c_void_p(hx.data_ptr()), self.M, self.K, int(hx.shape[1]),
+                 _p(self.x), self.ldx, _p(self.tiles), self.N, _p(b), _p(y), self.N,
+                 ctypes.c_void_p(y_host.data_ptr()), self.N, self.use_alpha, self.alpha, ctypes.byref(self.exact),
+                 _p(ws), ws.numel(), _p(self.flags), ctypes.c_void_p(f_host.data_ptr()), st.cuda_stream)
         done = torch.cuda.Event()
-        done.record(torch.cuda.current_stream(dev))
-        return DenseMatrix._streamed(self.y, y_host, f_host, done)
+        done.record(st)
+        return DenseMatrix._streamed(y, y_host, f_host, done)
 
     def pin_workspace(self) -> None:
         """Give this runner a private workspace (needed for graph capture / concurrent replays)."""
@@ -427,30 +435,53 @@ class GemmRunner:
         return int(f[2]) | (int(f[3]) << 32)
 
 
-def _x_operand(X, method: str) -> tuple[torch.Tensor, torch.Tensor | None]:
-    """Device buffer for X (DenseMatrix or PaddedInput) and, when X is still in
-    host memory and large enough to pay for chunking, the host tensor to stream
-    into it (GemmRunner.run_from_host, tensor-core path); otherwise X uploaded
-    whole and None."""
+_PLANS_PER_FORMAT = 4
+
+
+def _host_plan(kind: str, fmt, M: int, cols: int, method: str, kw: dict) -> GemmRunner:
+    """The cached host-streaming runner of ``fmt`` for this call shape (staging X,
+    workspace, status words and format reference built once; LRU of a few per
+    format, keyed by the stream too, so calls on different streams never share
+    a staging buffer)."""
+    dev = _device()
+    st = torch.cuda.current_stream(dev).cuda_stream
+    key = (kind, M, cols, method, kw.get("uf", 1), kw.get("mr", 1), kw.get("alpha"), dev.index, st)
+    plans = fmt.__dict__.setdefault("_host_plans", {})
+    r = plans.pop(key, None)
+    if r is None:
+        x = torch.empty((M, cols), dtype=torch.float32, device=dev)
+        r = GemmRunner(kind, x, fmt, None, method=method, out=False, **kw)
+        if len(plans) >= _PLANS_PER_FORMAT:
+            plans.pop(next(iter(plans)))
+    plans[key] = r  # most recently used last
+    return r
+
+
+def _dispatch(kind: str, X, fmt, bias: torch.Tensor, method: str, counted: bool, adds: int, **kw):
+    """Run one gemm_* call.  X still in host memory and large enough to pay for
+    chunking streams through the cached plan (tensor-core path,
+    GemmRunner.run_from_host); anything else is uploaded whole and launched."""
     if isinstance(X, PaddedInput):
         hs, cols = X._hsrc, X.K + 1
     else:
         hs, cols = _host_source(X._v), X.cols
     if method == "mma" and hs is not None and hs.numel() * 4 >= STREAM_MIN_BYTES and hs.shape[0] >= 128:
-        return torch.empty((int(hs.shape[0]), cols), dtype=torch.float32, device=_device()), hs
-    return X.device_values, None
-
-
-def _finish(runner: GemmRunner, counted: bool, adds: int, hx: torch.Tensor | None = None):
-    if hx is not None:
-        y = runner.run_from_host(hx)
-    else:
-        runner.launch()
-        y = runner.result()
+        with _plan_lock:
+            plan = _host_plan(kind, fmt, int(hs.shape[0]), cols, method, kw)
+            y = plan.run_from_host(hs, bias)
+        if not counted:
+            return y
+        return y, OpCount(int(adds), y._nonpositive() if plan.use_alpha else 0)
+    runner = GemmRunner(kind, X.device_values, fmt, bias, method=method, **kw)
+    runner.launch()
+    y = runner.result()
     if not counted:
         return y
     mults = runner.nonpositive() if runner.use_alpha else 0
     return y, OpCount(int(adds), int(mults))
+
+
+_plan_lock = threading.Lock()
 
 
 def _method(cfg: GemmConfig | None, method: str | None, K: int, N: int, nnz: int) -> str:
@@ -485,9 +516,7 @@ def gemm_base(X, t, b, counted: bool = False, *, method: str | None = None):
     X, b, t = as_dense(X), as_bias(b), _as_tcsc(t)
     _check_dims(X.cols, t.K, len(b), t.N)
     m = _method(None, method, t.K, t.N, t.nnz)
-    xd, hx = _x_operand(X, m)
-    r = GemmRunner("base", xd, t, b.device_values, method=m)
-    return _finish(r, counted, X.rows * t.N + X.rows * t.nnz, hx)
+    return _dispatch("base", X, t, b.device_values, m, counted, X.rows * t.N + X.rows * t.nnz)
 
 
 def gemm_unrolled(X, t, b, cfg: GemmConfig | None = None, counted: bool = False, *, method: str | None = None):
@@ -496,10 +525,8 @@ def gemm_unrolled(X, t, b, cfg: GemmConfig | None = None, counted: bool = False,
     X, b, t = as_dense(X), as_bias(b), _as_tcsc(t)
     _check_dims(X.cols, t.K, len(b), t.N)
     m = _method(cfg, method, t.K, t.N, t.nnz)
-    xd, hx = _x_operand(X, m)
-    r = GemmRunner("unrolled", xd, t, b.device_values, method=m, uf=cfg.uf)
     M = X.rows
-    return _finish(r, counted, M * t.nnz + M * t.N * (cfg.uf + 1), hx)
+    return _dispatch("unrolled", X, t, b.device_values, m, counted, M * t.nnz + M * t.N * (cfg.uf + 1), uf=cfg.uf)
 
 
 def gemm_blocked(X, t, b, cfg: GemmConfig | None = None, counted: bool = False, *, method: str | None = None):
@@ -508,11 +535,10 @@ def gemm_blocked(X, t, b, cfg: GemmConfig | None = None, counted: bool = False, 
     X, b, t = as_dense(X), as_bias(b), _as_blocked(t)
     _check_dims(X.cols, t.K, len(b), t.N)
     m = _method(cfg, method, t.K, t.N, t.nnz)
-    xd, hx = _x_operand(X, m)
-    r = GemmRunner("blocked", xd, t, b.device_values, method=m, uf=cfg.uf, mr=cfg.mr)
     M, nb = X.rows, t.num_blocks
     mf = M // cfg.mr * cfg.mr
-    return _finish(r, counted, M * t.nnz + mf * t.N * nb * (cfg.uf + 1) + (M - mf) * t.N * nb, hx)
+    adds = M * t.nnz + mf * t.N * nb * (cfg.uf + 1) + (M - mf) * t.N * nb
+    return _dispatch("blocked", X, t, b.device_values, m, counted, adds, uf=cfg.uf, mr=cfg.mr)
 
 
 def gemm_interleaved_blocked(X, t, b, cfg: GemmConfig | None = None, counted: bool = False, *,
@@ -526,10 +552,8 @@ def gemm_interleaved_blocked(X, t, b, cfg: GemmConfig | None = None, counted: bo
             "scalar kernel cannot consume symmetric-group formats (dummy index needs a padded input row)"
         )
     m = _method(cfg, method, t.K, t.N, t.nnz)
-    xd, hx = _x_operand(X, m)
-    r = GemmRunner("interleaved_blocked", xd, t, b.device_values, method=m)
     M = X.rows
-    return _finish(r, counted, M * t.nnz + M * t.N * t.num_blocks, hx)
+    return _dispatch("interleaved_blocked", X, t, b.device_values, m, counted, M * t.nnz + M * t.N * t.num_blocks)
 
 
 def gemm_vectorized_optimal(Xp, t, b, alpha: float | None = None, cfg: GemmConfig | None = None,
@@ -546,9 +570,8 @@ def gemm_vectorized_optimal(Xp, t, b, alpha: float | None = None, cfg: GemmConfi
     _alpha_args(alpha)
     n_idx = t._len("all_indices")
     m = _method(cfg, method, t.K, t.N, n_idx)
-    xd, hx = _x_operand(Xp, m)
-    r = GemmRunner("vectorized_optimal", xd, t, b.device_values, method=m, alpha=alpha)
-    return _finish(r, counted, Xp.M * (n_idx + t.N * t.num_blocks), hx)
+    adds = Xp.M * (n_idx + t.N * t.num_blocks)
+    return _dispatch("vectorized_optimal", Xp, t, b.device_values, m, counted, adds, alpha=alpha)
 
 
 def _as_sym(t) -> SymmetricInterleavedTcsc:
@@ -571,10 +594,8 @@ def _symmetric_kernel(kind: str, Xp, t, b, alpha, counted, method):
     _alpha_args(alpha)
     n_idx = t._len("indices")
     m = _method(None, method, t.K, t.N, n_idx)
-    xd, hx = _x_operand(Xp, m)
-    r = GemmRunner(kind, xd, t, b.device_values, method=m, alpha=alpha)
     extra = 2 if kind == "vertical" else 4  # simd.py:167-170 (b + p - q) / :253-256 (pairwise + b)
-    return _finish(r, counted, Xp.M * (n_idx + extra * t.N), hx)
+    return _dispatch(kind, Xp, t, b.device_values, m, counted, Xp.M * (n_idx + extra * t.N), alpha=alpha)
 
 
 def gemm_vertical(Xp, t, b, alpha: float | None = None, counted: bool = False, *, method: str | None = None):
@@ -598,10 +619,8 @@ def gemm_compressed(X, t, b, counted: bool = False, *, method: str | None = None
     if m == "auto":
         m = "mma" if t.K <= (1 << 24) else "gather"  # the code stream is dense: density gives no signal
     m = choose_method(m, t.K, t.N, t.K * t.N)
-    xd, hx = _x_operand(X, m)
-    r = GemmRunner("compressed", xd, t, b.device_values, method=m)
     nnz = t.nnz if counted else 0
-    return _finish(r, counted, X.rows * nnz + X.rows * t.N, hx)
+    return _dispatch("compressed", X, t, b.device_values, m, counted, X.rows * nnz + X.rows * t.N)
 
 
 # ---------------------------------------------------------------- registry (kernels/__init__.py:66-230)

@@ -120,7 +120,8 @@ def test_wide_rows_without_exact_format_use_fp64(tg):
         assert err <= TOL, (m, err)
 
 
-def test_nonfinite_input_is_reported(tg):
+@pytest.mark.parametrize("bad", [float("inf"), float("-inf"), float("nan")])
+def test_nonfinite_input_is_reported(tg, bad):
     """A non-finite X entry (the reference rejects it when constructing DenseMatrix,
     dense.py:77) is flagged by the tensor-core split and raised on first host access."""
     from paper_2510_06957_b200.errors import ParameterError
@@ -128,7 +129,7 @@ def test_nonfinite_input_is_reported(tg):
     M, K, N = 20, 256, 128
     W = torch.randint(-1, 2, (K, N), device="cuda", dtype=torch.int8)
     X = torch.randn((M, K), device="cuda")
-    X[5, 7] = float("inf")
+    X[5, 7] = bad
     t = tg.tcsc_from_dense(tg.TernaryDense(W))
     with pytest.raises(ParameterError):
         tg.gemm_base(X, t, torch.zeros(N, device="cuda"), method="mma").values
@@ -168,3 +169,40 @@ def test_host_input_is_streamed_bit_exact(tg, method):
             y = call(x)
             assert np.array_equal(y.values, ref), (i, type(x))
             assert torch.equal(y.device_values.cpu(), torch.from_numpy(ref))
+
+
+def test_host_streaming_graph_replay(tg):
+    """Repeated host-streamed calls replay the library's CUDA graph of the first
+    (same pointers): new X contents in the same pinned buffer, results kept
+    alive (new Y pointers: a fresh capture), counted mode, a side stream, and a
+    non-finite X in a replay must all behave exactly like the direct enqueue."""
+    from paper_2510_06957_b200.errors import ParameterError
+
+    M, K, N = 512, 1024, 512
+    rng = np.random.default_rng(11)
+    W = rng.integers(-1, 2, size=(K, N)).astype(np.int8)
+    b = rng.standard_normal(N).astype(np.float32)
+    Wd = torch.from_numpy(W).cuda()
+    ibs = tg.interleaved_blocked_from_dense(Wd, None, 2, True)
+    Xpin = torch.empty((M, K)).pin_memory()
+    kept = []
+    for it in range(6):
+        X = rng.standard_normal((M, K)).astype(np.float32)
+        Xpin.copy_(torch.from_numpy(X))
+        yr, ops_ref = tg.gemm_vectorized_optimal(tg.pad_input(torch.from_numpy(X).cuda()), ibs, b, 0.25,
+                                                 counted=True)
+        ref = yr.values.copy()
+        y, ops = tg.gemm_vectorized_optimal(tg.pad_input(Xpin), ibs, b, 0.25, counted=True)
+        assert np.array_equal(y.values, ref), it
+        assert ops == ops_ref, (it, ops, ops_ref)
+        if it % 2:
+            kept.append(y)  # Y stays alive: the next call gets another device Y
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        y2 = tg.gemm_vectorized_optimal(tg.pad_input(Xpin), ibs, b, 0.25).values
+    assert np.array_equal(y2, ref)
+    Xpin[100, 3] = float("nan")
+    with pytest.raises(ParameterError):
+        tg.gemm_vectorized_optimal(tg.pad_input(Xpin), ibs, b, 0.25).values
+    Xpin[100, 3] = 0.0
+    assert np.isfinite(tg.gemm_vectorized_optimal(tg.pad_input(Xpin), ibs, b, 0.25).values).all()

@@ -175,7 +175,7 @@ def test_c_abi_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
     assert set(names) == set(_native.SIGNATURES), set(names) ^ set(_native.SIGNATURES)
     L = _native.load()
-    assert L.tg_abi_version() == 3
+    assert L.tg_abi_version() == 4
     # pure size queries need no device
     assert L.tg_tiles_bytes(4096, 4096) == 32 * 4096 * 8 * 4
     assert L.tg_build_workspace_bytes(4096, 4096, 4096) > 0
