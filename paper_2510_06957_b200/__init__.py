@@ -7,7 +7,18 @@ GEMM variants and the variant registry — backed by hand-written sm_100a CUDA
 (csrc/) behind the C ABI in include/terngemm_b200.h.  There is no CPU path.
 """
 
-from .dense import BiasVector, DenseMatrix, TernaryDense, oracle_gemm, prelu
+from .dense import (
+    BiasVector,
+    DenseMatrix,
+    TernaryDense,
+    as_fraction,
+    gen_bias,
+    gen_input,
+    gen_input_uniform,
+    gen_ternary,
+    oracle_gemm,
+    prelu,
+)
 from .errors import CorruptionError, InvalidCodeError, ParameterError, ParseError, VerificationError
 from .formats import (
     CODE_COUNT,
@@ -55,6 +66,8 @@ from .kernels import (
     run_variant,
 )
 
+from . import io  # noqa: E402  (TGW1 / TGS1 files, io.py)
+
 __version__ = "0.1.0"
 
 __all__ = [
@@ -68,4 +81,5 @@ __all__ = [
     "gemm_unrolled", "gemm_vectorized_optimal", "get_variant", "interleaved_blocked_from_dense",
     "operational_intensity", "oracle_gemm", "pad_input", "prelu", "resolve_block_size", "run_variant",
     "tcsc_bytes_for", "tcsc_from_dense", "tcsc_to_dense", "validate", "__version__",
+    "as_fraction", "gen_bias", "gen_input", "gen_input_uniform", "gen_ternary", "io",
 ]

@@ -1016,7 +1016,13 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
         if (p.sig_local) peer_copy_tile<MT>(p, ytile, m0, n0, et, ET);  // overlaps the local TMA store
       }
     }
-    if (et == 0 && p.tma_y) bulk_wait_group0();
+    // the smem tile must have been read before the CTA exits; the global writes complete
+    // with the grid (as CUTLASS's store tail).  The peer path keeps the full wait: its
+    // arrival signal below must follow this rank's own Y as well.
+    if (et == 0 && p.tma_y) {
+      if (p.sig_local) bulk_wait_group0();
+      else bulk_wait_group_read0();
+    }
     if (p.sig_local) {
       // the last CTA to finish tells every rank that this rank's shard is in place
       __threadfence_system();  // this thread's peer stores before the CTA's arrival

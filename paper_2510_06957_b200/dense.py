@@ -13,6 +13,7 @@ path never synchronises.
 from __future__ import annotations
 
 import threading
+from fractions import Fraction
 import weakref
 
 import numpy as np
@@ -360,3 +361,64 @@ def oracle_gemm(X, W, b, alpha: float | None = None) -> DenseMatrix:
     if alpha is not None:
         y = torch.where(y > 0, y, float(alpha) * y)
     return DenseMatrix(y.float())
+
+
+# ---------------------------------------------------------------- seeded generators (dense.py:24-181)
+# Host-side input generators with the reference's exact recipes, so files and
+# `verify` runs made with either package hold the same matrices for a seed.
+
+DEFAULT_INT_RANGE = 8  # dense.py:21
+
+
+def as_fraction(s) -> Fraction:
+    """dense.py:24-29."""
+    frac = Fraction(s)
+    if not 0 < frac <= 1:
+        raise ParameterError(f"sparsity must lie in (0, 1], got {s!r}")
+    return frac
+
+
+def gen_ternary(K: int, N: int, s, seed: int) -> TernaryDense:
+    """dense.py:112-140: every column gets exactly round(s*K) nonzeros at
+    rng.choice positions, the first ceil(nz/2) of them +1, the rest -1."""
+    if K < 1 or N < 1:
+        raise ParameterError(f"K and N must be >= 1, got K={K} N={N}")
+    nz = round(as_fraction(s) * K)
+    if nz > K:
+        raise ParameterError(f"round(s*K) = {nz} exceeds K = {K}")
+    n_pos = (nz + 1) // 2
+    rng = np.random.default_rng(seed)
+    w = np.zeros((K, N), dtype=np.int8)
+    for n in range(N):
+        chosen = rng.choice(K, size=nz, replace=False)
+        w[chosen[:n_pos], n] = 1
+        w[chosen[n_pos:], n] = -1
+    return TernaryDense(w)
+
+
+def gen_input(M: int, K: int, seed: int, int_range: int = DEFAULT_INT_RANGE) -> DenseMatrix:
+    """dense.py:143-162: integers uniform in [-int_range, int_range] (exact fp32 sums)."""
+    if M < 1 or K < 1:
+        raise ParameterError(f"M and K must be >= 1, got M={M} K={K}")
+    if int_range < 1:
+        raise ParameterError(f"int_range must be >= 1, got {int_range}")
+    if K * int_range >= EXACT_FLOAT32_BOUND:
+        raise ParameterError(f"K * int_range = {K * int_range} >= 2**24 would break exact float32 accumulation")
+    rng = np.random.default_rng(seed)
+    return DenseMatrix(rng.integers(-int_range, int_range + 1, size=(M, K)).astype(np.float32))
+
+
+def gen_input_uniform(M: int, K: int, seed: int) -> DenseMatrix:
+    """dense.py:165-175: uniform [-1, 1) drawn in fp64, cast to fp32."""
+    if M < 1 or K < 1:
+        raise ParameterError(f"M and K must be >= 1, got M={M} K={K}")
+    rng = np.random.default_rng(seed)
+    return DenseMatrix((rng.random(size=(M, K), dtype=np.float64) * 2.0 - 1.0).astype(np.float32))
+
+
+def gen_bias(N: int, seed: int, int_range: int = DEFAULT_INT_RANGE) -> BiasVector:
+    """dense.py:178-181."""
+    if N < 1:
+        raise ParameterError(f"N must be >= 1, got N={N}")
+    rng = np.random.default_rng(seed)
+    return BiasVector(rng.integers(-int_range, int_range + 1, size=N).astype(np.float32))

@@ -207,7 +207,46 @@ def cfg1_fixture():
     print("cfg1.npz: nnz", t.nnz)
 
 
+def files_fixture():
+    """TGW1 / TGS1 bytes written by the reference (io.py) and its seeded generators."""
+    import io as _io
+
+    from terngemm import io as tio
+
+    def dump(fn, obj):
+        fh = _io.BytesIO()
+        fn(obj, fh)
+        return np.frombuffer(fh.getvalue(), dtype=np.uint8)
+
+    store = {}
+    meta = []
+    for i, (K, N, s, seed) in enumerate([(24, 8, "1/2", 6), (37, 12, "1/4", 1), (130, 20, "3/5", 2), (9, 4, "1", 3)]):
+        w = tg.gen_ternary(K, N, s, seed)
+        store[f"f{i}_W"] = w.values
+        store[f"f{i}_dense"] = dump(tio.save_dense, w)
+        fmts = {
+            "tcsc": tg.tcsc_from_dense(w),
+            "blocked": tg.blocked_from_dense(w, B=8),
+            "interleaved_blocked": tg.interleaved_blocked_from_dense(w, B=8, g=2),
+            "compressed": tg.compressed_from_dense(w),
+        }
+        if N % 4 == 0:
+            fmts["interleaved_blocked_sym"] = tg.interleaved_blocked_from_dense(w, B=8, g=2, symmetric_cols=True)
+            fmts["symmetric"] = tg.symmetric_from_dense(w, g=2)
+        for name, fmt in fmts.items():
+            store[f"f{i}_{name}"] = dump(tio.save_sparse, fmt)
+        store[f"f{i}_interleaved"] = dump(tio.save_sparse, tg.interleaved_from_dense(w, g=2))  # not supported here
+        meta.append({"K": K, "N": N, "s": s, "seed": seed, "formats": sorted(fmts)})
+        store[f"f{i}_gen_input"] = tg.gen_input(5, K, seed + 1).values
+        store[f"f{i}_gen_bias"] = tg.gen_bias(N, seed + 2).values
+        store[f"f{i}_gen_uniform"] = tg.gen_input_uniform(3, K, seed).values
+    store["meta"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(HERE, "files.npz"), **store)
+    print("files.npz:", len(meta), "matrices")
+
+
 if __name__ == "__main__":
+    files_fixture()
     formats_fixture()
     kernels_fixture()
     cfg1_fixture()
