@@ -178,7 +178,7 @@ int tg_gemm_tiles_prepare(const float* X, int64_t M, int64_t K, int64_t ldx, voi
 static int gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N,
                           const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha,
                           const tg_format_ref* exact, const tg_peer_scatter* sc, void* ws, size_t ws_bytes,
-                          tg_device_flags* flags, void* stream) {
+                          tg_device_flags* flags, void* stream, int share = 1) {
   TG_REQUIRE(M >= 1 && K >= 1 && N >= 1, TG_ERR_PARAM, "M, K and N must be >= 1");
   TG_REQUIRE(ldy >= N && ldx >= K, TG_ERR_PARAM, "leading dimensions too small");
   TG_REQUIRE(tiles && Y && ws && X, TG_ERR_PARAM, "null pointer");
@@ -192,10 +192,10 @@ static int gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, con
     TG_REQUIRE(exact->B >= 1 && exact->g >= 1 && exact->uf >= 1 && exact->mr >= 1, TG_ERR_PARAM,
                "exact format: B, g, uf, mr must be >= 1");
   }
-  TG_REQUIRE(ws_bytes >= mma_ws_bytes(M, K, N), TG_ERR_PARAM, "workspace too small");
+  TG_REQUIRE(ws_bytes >= mma_ws_bytes(M, K, N, share), TG_ERR_PARAM, "workspace too small");
   TG_TRY(require_device());
   if (!exact) return run_mma(X, M, K, ldx, tiles, N, bias, Y, ldy, use_alpha, alpha, nullptr, ws, ws_bytes, flags,
-                             as_stream(stream), sc);
+                             as_stream(stream), sc, share);
   const int v = exact->variant;
   MmaFixup fx{};
   const int64_t nb = (v == TG_VARIANT_BASE || v == TG_VARIANT_UNROLLED) ? 1 : ceil_div(K, exact->B);
@@ -215,7 +215,7 @@ static int gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, con
                          v == TG_VARIANT_BASE ? 1 : exact->uf, nullptr, 0};
   }
   return run_mma(X, M, K, ldx, tiles, N, bias, Y, ldy, use_alpha, alpha, &fx, ws, ws_bytes, flags,
-                 as_stream(stream), sc);
+                 as_stream(stream), sc, share);
 }
 
 int tg_gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N,
@@ -302,10 +302,14 @@ int tg_gemm_tiles(const float* X, int64_t M, int64_t K, int64_t ldx, const uint3
 // ------------------------------------------------------------------ GEMM from host memory
 namespace {
 
-// Row chunks of a host-resident X: about 512 KB of X each, at most 8, starting
+// Row chunks of a host-resident X: about 2 MB of X each, at most 8, starting
 // at multiples of 64 rows (a multiple of every blocked-order row unroll mr).
 // Small chunks let the two PCIe directions and the GEMMs overlap; what they
-// cost in host work is paid once, when the call is captured in a graph.
+// cost in host work is paid once, when the call is captured in a graph.  The
+// chunks on the P.streams side streams run their GEMMs side by side, each on
+// 1/P.streams of the SMs: a chunk's GEMM costs about as long as the whole
+// one (its fill, epilogue and W stream do not shrink with the rows), so run
+// one after another they would serialise the pipeline.
 struct HostPlan {
   int64_t rows, n;  // chunk height (the last one may be shorter), chunk count
   int streams;      // side streams used
@@ -316,22 +320,25 @@ HostPlan host_plan(int64_t M, int64_t K, int64_t N) {
   HostPlan P;
   const int64_t bytes = M * K * 4;
   int64_t cap = 8;
-  if (const char* env = getenv("TG_HOST_CHUNKS")) cap = std::max(1, atoi(env));
-  int64_t n = std::max<int64_t>(1, std::min<int64_t>({cap, bytes >> 19, M / 64}));
+  if (const char* env = getenv("TG_HOST_CHUNKS")) cap = std::min(8, std::max(1, atoi(env)));  // (8 chunk events)
+  int64_t n = std::max<int64_t>(1, std::min<int64_t>({cap, bytes >> 21, M / 64}));
   P.rows = round_up(ceil_div(M, n), 64);
   P.n = ceil_div(M, P.rows);
   P.streams = int(std::min<int64_t>(P.n, 4));
   const int64_t last = M - (P.n - 1) * P.rows;
-  P.ws_slice = size_t(round_up(int64_t(std::max(mma_ws_bytes(P.rows, K, N), mma_ws_bytes(last, K, N))), 256));
+  P.ws_slice = size_t(round_up(
+      int64_t(std::max(mma_ws_bytes(P.rows, K, N, P.streams), mma_ws_bytes(last, K, N, P.streams))), 256));
   return P;
 }
 
 // The library's own side streams and events, per device (created once), and
 // the stream host-streaming calls are captured on.
 struct SideStreams {
-  cudaStream_t s[4];
+  cudaStream_t s[4];       // chunk GEMMs (chunk c on s[c % 4])
+  cudaStream_t cin, cout;  // the X chunks in, the Y chunks out, each in chunk order
   cudaEvent_t join[4];
-  cudaEvent_t fork;
+  cudaEvent_t xin[8], ydone[8];  // chunk c: X landed / Y computed
+  cudaEvent_t fork, join_in, join_out;
   cudaStream_t capture;
 };
 
@@ -350,7 +357,15 @@ int side_streams(SideStreams** out) {
           (e = cudaEventCreateWithFlags(&ss.join[i], cudaEventDisableTiming)) != cudaSuccess)
         return set_cuda_error(e, "side stream creation");
     }
+    for (int i = 0; i < 8; ++i)
+      if ((e = cudaEventCreateWithFlags(&ss.xin[i], cudaEventDisableTiming)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&ss.ydone[i], cudaEventDisableTiming)) != cudaSuccess)
+        return set_cuda_error(e, "side stream creation");
     if ((e = cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ss.join_in, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ss.join_out, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&ss.cin, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&ss.cout, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaStreamCreateWithFlags(&ss.capture, cudaStreamNonBlocking)) != cudaSuccess)
       return set_cuda_error(e, "side stream creation");
     it = per_dev.emplace(dev, ss).first;
@@ -395,6 +410,25 @@ struct HostGraph {
 
 constexpr int kHostGraphs = 16;
 
+#ifdef TG_TRACE
+// [chunk][0 = H2D done, 1 = GEMM done, 2 = D2H done] + the fork, recorded on direct enqueues
+cudaEvent_t g_host_ev[16][3];
+cudaEvent_t g_host_ev0;
+int g_host_nev = 0;
+#define TG_HOST_EV(c, j, st)                                                                  \
+  do {                                                                                        \
+    if ((c) < 16) {                                                                           \
+      if (!g_host_ev[c][j]) cudaEventCreate(&g_host_ev[c][j]);                                \
+      cudaEventRecord(g_host_ev[c][j], st);                                                   \
+      g_host_nev = int(c) + 1;                                                                \
+    }                                                                                         \
+  } while (0)
+#else
+#define TG_HOST_EV(c, j, st) \
+  do {                       \
+  } while (0)
+#endif
+
 int enqueue_host(const HostKey& k, const HostPlan& P, SideStreams* ss, cudaStream_t main) {
   cudaError_t e;
   if (k.flags_host && (e = cudaMemsetAsync(k.flags, 0, sizeof(tg_device_flags), main)) != cudaSuccess)
@@ -404,35 +438,65 @@ int enqueue_host(const HostKey& k, const HostPlan& P, SideStreams* ss, cudaStrea
     if (e != cudaSuccess) return set_cuda_error(e, "cudaMemset2DAsync(padded slot)");
   }
   if ((e = cudaEventRecord(ss->fork, main)) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
+#ifdef TG_TRACE
+  if (!g_host_ev0) cudaEventCreate(&g_host_ev0);
+  cudaEventRecord(g_host_ev0, main);
+#endif
+  // Copies go through two in-order streams: issued from independent streams (or
+  // as independent graph nodes) the copy engines may take the chunks in any
+  // order or interleave them, and the first chunk's GEMM then starts last.
   for (int i = 0; i < P.streams; ++i)
     if ((e = cudaStreamWaitEvent(ss->s[i], ss->fork, 0)) != cudaSuccess) return set_cuda_error(e, "fork");
+  if ((e = cudaStreamWaitEvent(ss->cin, ss->fork, 0)) != cudaSuccess ||
+      (e = cudaStreamWaitEvent(ss->cout, ss->fork, 0)) != cudaSuccess)
+    return set_cuda_error(e, "fork");
   const tg_format_ref* exact = k.has_exact ? &k.exact : nullptr;
   const int64_t M = k.M, K = k.K, N = k.N;
-  for (int64_t c = 0; c < P.n; ++c) {
+  for (int64_t c = 0; c < P.n; ++c) {  // X chunks in, in order
+    const int64_t r0 = c * P.rows, rows = std::min(P.rows, M - r0);
+    float* xd = k.X_dev + r0 * k.ldx_dev;
+    e = k.ldx_dev == K && k.ldx_host == K
+            ? cudaMemcpyAsync(xd, k.X_host + r0 * K, size_t(rows * K) * 4, cudaMemcpyHostToDevice, ss->cin)
+            : cudaMemcpy2DAsync(xd, size_t(k.ldx_dev) * 4, k.X_host + r0 * k.ldx_host, size_t(k.ldx_host) * 4,
+                                size_t(K) * 4, size_t(rows), cudaMemcpyHostToDevice, ss->cin);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaMemcpy2DAsync(X chunk)");
+    if ((e = cudaEventRecord(ss->xin[c], ss->cin)) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
+    TG_HOST_EV(c, 0, ss->cin);
+  }
+  for (int64_t c = 0; c < P.n; ++c) {  // GEMMs side by side, each on 1/P.streams of the SMs
     const int i = int(c % P.streams);
     cudaStream_t st = ss->s[i];
     const int64_t r0 = c * P.rows, rows = std::min(P.rows, M - r0);
     float* xd = k.X_dev + r0 * k.ldx_dev;
     float* yd = k.Y_dev + r0 * k.ldy_dev;
     void* wsi = static_cast<uint8_t*>(k.ws) + size_t(i) * P.ws_slice;
-    e = k.ldx_dev == K && k.ldx_host == K
-            ? cudaMemcpyAsync(xd, k.X_host + r0 * K, size_t(rows * K) * 4, cudaMemcpyHostToDevice, st)
-            : cudaMemcpy2DAsync(xd, size_t(k.ldx_dev) * 4, k.X_host + r0 * k.ldx_host, size_t(k.ldx_host) * 4,
-                                size_t(K) * 4, size_t(rows), cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaMemcpy2DAsync(X chunk)");
+    if ((e = cudaStreamWaitEvent(st, ss->xin[c], 0)) != cudaSuccess) return set_cuda_error(e, "wait X chunk");
     TG_TRY(tg_gemm_tiles_prepare(xd, rows, K, k.ldx_dev, wsi, P.ws_slice, k.flags, st));
     TG_TRY(gemm_tiles_run(xd, rows, K, k.ldx_dev, k.tiles, N, k.bias, yd, k.ldy_dev, k.use_alpha, k.alpha, exact,
-                          nullptr, wsi, P.ws_slice, k.flags, st));
+                          nullptr, wsi, P.ws_slice, k.flags, st, P.streams));
+    if ((e = cudaEventRecord(ss->ydone[c], st)) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
+    TG_HOST_EV(c, 1, st);
+  }
+  for (int64_t c = 0; c < P.n; ++c) {  // Y chunks out, in order
+    const int64_t r0 = c * P.rows, rows = std::min(P.rows, M - r0);
+    const float* yd = k.Y_dev + r0 * k.ldy_dev;
+    if ((e = cudaStreamWaitEvent(ss->cout, ss->ydone[c], 0)) != cudaSuccess) return set_cuda_error(e, "wait Y");
     e = k.ldy_dev == N && k.ldy_host == N
-            ? cudaMemcpyAsync(k.Y_host + r0 * N, yd, size_t(rows * N) * 4, cudaMemcpyDeviceToHost, st)
+            ? cudaMemcpyAsync(k.Y_host + r0 * N, yd, size_t(rows * N) * 4, cudaMemcpyDeviceToHost, ss->cout)
             : cudaMemcpy2DAsync(k.Y_host + r0 * k.ldy_host, size_t(k.ldy_host) * 4, yd, size_t(k.ldy_dev) * 4,
-                                size_t(N) * 4, size_t(rows), cudaMemcpyDeviceToHost, st);
+                                size_t(N) * 4, size_t(rows), cudaMemcpyDeviceToHost, ss->cout);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaMemcpy2DAsync(Y chunk)");
+    TG_HOST_EV(c, 2, ss->cout);
   }
   for (int i = 0; i < P.streams; ++i) {
     if ((e = cudaEventRecord(ss->join[i], ss->s[i])) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
     if ((e = cudaStreamWaitEvent(main, ss->join[i], 0)) != cudaSuccess) return set_cuda_error(e, "join");
   }
+  if ((e = cudaEventRecord(ss->join_in, ss->cin)) != cudaSuccess ||
+      (e = cudaEventRecord(ss->join_out, ss->cout)) != cudaSuccess ||
+      (e = cudaStreamWaitEvent(main, ss->join_in, 0)) != cudaSuccess ||
+      (e = cudaStreamWaitEvent(main, ss->join_out, 0)) != cudaSuccess)
+    return set_cuda_error(e, "join");
   if (k.flags_host &&
       (e = cudaMemcpyAsync(k.flags_host, k.flags, sizeof(tg_device_flags), cudaMemcpyDeviceToHost, main)) !=
           cudaSuccess)
@@ -458,6 +522,16 @@ cudaGraphExec_t capture_host(const HostKey& k, const HostPlan& P, SideStreams* s
 }
 
 }  // namespace
+
+#ifdef TG_TRACE
+// ms since the fork of the last direct host-streaming call: out[3 c + j]; returns the chunk count
+extern "C" int tg_debug_host_trace(float* out) {
+  cudaDeviceSynchronize();
+  for (int c = 0; c < g_host_nev; ++c)
+    for (int j = 0; j < 3; ++j) cudaEventElapsedTime(&out[3 * c + j], g_host_ev0, g_host_ev[c][j]);
+  return g_host_nev;
+}
+#endif
 
 extern "C" {
 

@@ -20,7 +20,7 @@ inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
 struct GatherArgs;  // tg_walk.cuh
 int mma_pick_mt(int64_t M);
 size_t xsplit_bytes(int64_t M, int64_t K);
-size_t mma_ws_bytes(int64_t M, int64_t K, int64_t N);
+size_t mma_ws_bytes(int64_t M, int64_t K, int64_t N, int share = 1);
 int run_xsplit(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size_t ws_bytes, tg_device_flags* flags,
                cudaStream_t st);
 int run_pack_dense(const int8_t* W, int64_t K, int64_t N, int64_t ldw, uint32_t* tiles, tg_device_flags* flags,
@@ -63,5 +63,5 @@ int run_pack_sym(const int32_t* idx, const int32_t* ptr, int64_t N, int g, int64
 int run_pack_codes(const uint8_t* codes, int64_t K, int64_t N, uint32_t* tiles, cudaStream_t st);
 int run_mma(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N, const float* bias,
             float* Y, int64_t ldy, int use_alpha, float alpha, const MmaFixup* fix, void* ws, size_t ws_bytes,
-            tg_device_flags* flags, cudaStream_t st, const tg_peer_scatter* sc = nullptr);
+            tg_device_flags* flags, cudaStream_t st, const tg_peer_scatter* sc = nullptr, int share = 1);
 }  // namespace tg

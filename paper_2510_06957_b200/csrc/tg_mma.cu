@@ -379,7 +379,7 @@ struct MmaParams {
   const float* bias;       // [N] or null
   float* Y;
   int64_t ldy;
-  int M, N, KC, KS, M_pad, N_pad, MB, NB, splits;  // KC 128-k chunks, KS = ceil(KC/2) stages
+  int M, N, K, KC, KS, M_pad, N_pad, MB, NB, splits;  // KC 128-k chunks, KS = ceil(KC/2) stages
   int NBG;                 // column-block groups: one group of CS blocks per cluster unit
   int units;               // cluster units = MB * NBG * splits
   int use_alpha;
@@ -991,7 +991,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
             bits &= bits - 1;
             const int m = m0 + j;
             if (m >= p.M || ((j >> 4) & 1) != half) continue;
-            float y = column_value_row(p.fix_var, p.fix, n, bf, p.X + int64_t(m) * p.ldx, m < p.m_full);
+            float y = column_value_row(p.fix_var, p.fix, n, bf, p.X + int64_t(m) * p.ldx, p.K, m < p.m_full);
             if (p.use_alpha && !(y > 0.f)) {
               y = p.alpha * y;
               ++npos;
@@ -1327,7 +1327,10 @@ struct SplitLayout {
   size_t off_rscale, off_counters, off_part, total_prepare, total;
 };
 
-static SplitLayout split_layout(int64_t M, int64_t K, int64_t N) {
+// `share` > 1: this GEMM runs beside share - 1 others (host streaming's row chunks on
+// their own streams) and takes 1/share of the co-resident clusters, so the chunks'
+// GEMMs run side by side on disjoint SMs instead of one after another.
+static SplitLayout split_layout(int64_t M, int64_t K, int64_t N, int share = 1) {
   SplitLayout L;
   L.mt = mma_pick_mt(M);
   L.M_pad = round_up(M, L.mt);
@@ -1338,7 +1341,7 @@ static SplitLayout split_layout(int64_t M, int64_t K, int64_t N) {
   L.NB = L.N_pad / 128;
   L.cs = N > 0 ? pick_cluster(L.mt, L.NB) : 1;
   L.NBG = ceil_div(L.NB, L.cs);
-  L.clusters = N > 0 ? max_clusters_for(L.mt, L.cs) : 1;
+  L.clusters = N > 0 ? std::max(1, max_clusters_for(L.mt, L.cs) / std::max(1, share)) : 1;
   L.splits = N > 0 ? pick_splits(L.MB * L.NBG, ceil_div(L.KC, 2), L.clusters) : 1;
   L.off_rscale = size_t(round_up(3 * L.M_pad * L.K_pad, 256));
   L.total_prepare = L.off_rscale + size_t(round_up(L.M_pad * int64_t(sizeof(double)), 256));
@@ -1350,7 +1353,7 @@ static SplitLayout split_layout(int64_t M, int64_t K, int64_t N) {
 }
 
 size_t xsplit_bytes(int64_t M, int64_t K) { return split_layout(M, K, 0).total_prepare; }
-size_t mma_ws_bytes(int64_t M, int64_t K, int64_t N) { return split_layout(M, K, N).total; }
+size_t mma_ws_bytes(int64_t M, int64_t K, int64_t N, int share) { return split_layout(M, K, N, share).total; }
 
 int run_xsplit(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size_t ws_bytes, tg_device_flags* flags,
                cudaStream_t st) {
@@ -1438,8 +1441,8 @@ static int launch_mma(const CUtensorMap& map, const CUtensorMap& ymap, const Mma
 
 int run_mma(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N, const float* bias,
             float* Y, int64_t ldy, int use_alpha, float alpha, const MmaFixup* fix, void* ws, size_t ws_bytes,
-            tg_device_flags* flags, cudaStream_t st, const tg_peer_scatter* sc) {
-  const SplitLayout L = split_layout(M, K, N);
+            tg_device_flags* flags, cudaStream_t st, const tg_peer_scatter* sc, int share) {
+  const SplitLayout L = split_layout(M, K, N, share);
   if (ws_bytes < L.total) return set_error(TG_ERR_PARAM, "workspace too small for the tensor-core path");
   uint8_t* base = static_cast<uint8_t*>(ws);
   int8_t* limbs = reinterpret_cast<int8_t*>(base);
@@ -1481,6 +1484,7 @@ int run_mma(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* t
   p.ldy = ldy;
   p.M = int(M);
   p.N = int(N);
+  p.K = int(K);
   p.KC = int(L.KC);
   p.KS = int(ceil_div(L.KC, 2));
   p.M_pad = int(L.M_pad);

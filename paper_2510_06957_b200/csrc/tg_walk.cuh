@@ -84,10 +84,11 @@ struct SrcXt {  // 4 consecutive rows from the transposed copy Xt[K+1][M_pad]
   int64_t ld;
   __device__ __forceinline__ float4 operator()(int32_t k) const { return ld4(xt + int64_t(k) * ld); }
 };
-struct SrcRow {  // one row of X in place (ldx = K or K+1)
-  using V = float;
+struct SrcRow {  // one row of X in place; the padded slot k = K reads as the exact zero it holds
+  using V = float;  // (simd.py:72-75), so the row needs no slot column (a contiguous [M, K] X works)
   const float* x;
-  __device__ __forceinline__ float operator()(int32_t k) const { return __ldg(x + k); }
+  int32_t K;
+  __device__ __forceinline__ float operator()(int32_t k) const { return k < K ? __ldg(x + k) : 0.f; }
 };
 // Walk [a, b) of an index stream adding (NEG=false) or subtracting into acc,
 // strictly in stream order.
@@ -250,8 +251,8 @@ __device__ __forceinline__ typename S::V column_value(const GatherArgs& a, int64
 
 // Runtime dispatch of the one-row (SrcRow) evaluation, for the fix-up paths.
 __device__ __forceinline__ float column_value_row(int var, const GatherArgs& a, int64_t n, float b, const float* xrow,
-                                                  bool banked) {
-  const SrcRow src{xrow};
+                                                  int32_t K, bool banked) {
+  const SrcRow src{xrow, K};
   const unsigned br = banked ? 1u : 0u;
   switch (var) {
     case VAR_BASE: return column_value<VAR_BASE>(a, n, b, src, br);

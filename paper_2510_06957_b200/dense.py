@@ -68,6 +68,28 @@ class _PinnedPool:
 _pinned = _PinnedPool()
 
 
+class _EventPool:
+    """Recycled CUDA events for streamed results (creating one costs a few us)."""
+
+    def __init__(self):
+        self._free: list[torch.cuda.Event] = []
+        self._lock = threading.Lock()
+
+    def take(self) -> torch.cuda.Event:
+        with self._lock:
+            if self._free:
+                return self._free.pop()
+        return torch.cuda.Event()
+
+    def give(self, e: torch.cuda.Event) -> None:
+        with self._lock:
+            if len(self._free) < 16:
+                self._free.append(e)
+
+
+_events = _EventPool()
+
+
 def _to_host(d: torch.Tensor, extra: torch.Tensor | None = None):
     """Device -> host through pinned memory (one stream-ordered async copy, one
     synchronisation); ``extra`` (a small status tensor) rides along and is
@@ -219,6 +241,7 @@ class DenseMatrix:
     def _arrive(self) -> None:
         host, done = self._arrival
         done.synchronize()
+        _events.give(done)
         self._arrival = None
         f = self._flags
         self._flags = f.clone()

@@ -90,7 +90,11 @@ class _Format:
         return self._a[name].dev()
 
     def _len(self, name: str) -> int:
-        return int(np.prod(self._a[name].shape()))
+        lens = self.__dict__.setdefault("_lens", {})  # the arrays never change size
+        n = lens.get(name)
+        if n is None:
+            n = lens[name] = int(np.prod(self._a[name].shape()))
+        return n
 
     def format_bytes(self) -> int:
         return 4 * sum(self._len(n) for n in self._arrays)
