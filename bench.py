@@ -474,6 +474,8 @@ def run_ours(args) -> None:
         e1.record(stream)
         e1.synchronize()
         t_e2e.append(e0.elapsed_time(e1))
+    if t_e2e and os.environ.get("BENCH_E2E_SAMPLES"):
+        print("e2e samples (ms):", " ".join(f"{t:.4f}" for t in t_e2e), file=sys.stderr)
     t_e2e_ms = max_over_ranks(sum(t_e2e) / len(t_e2e), world, dev) if t_e2e else float("nan")
     e2e_value = total_ops / (t_e2e_ms * 1e-3) / 1e9 if t_e2e else None
 

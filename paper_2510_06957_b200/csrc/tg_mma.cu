@@ -87,6 +87,17 @@ constexpr float kWideRatio = 16.f;
 // (and every partial product) far inside the fp32 range.  Rows outside take the
 // exact-order path.
 constexpr int kMaxScaleExp = 100;
+// Split-K arrival counters (one per (row block, column block) tile) live right after
+// the row scales.  The X split zeroes them, so the tile GEMM needs no memset node
+// between the two kernels (that node costs ~6 us and the programmatic overlap);
+// the last-arriving unit of a tile resets its counter for replays.  Split-K is only
+// used while the tiles fit (split_layout).
+constexpr int kSplitCounters = 4096;
+__device__ __forceinline__ void zero_split_counters(double* rscale, int64_t M_pad) {
+  int32_t* c = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(rscale) + ((M_pad * 8 + 255) / 256) * 256);
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < kSplitCounters) c[i] = 0;
+}
 constexpr int64_t XS_SMEM_MAX_K = 16384;  // rows up to 64 KB are staged in shared memory
 
 // max that propagates NaN (fmaxf drops it), so a NaN anywhere in a row makes
@@ -141,6 +152,7 @@ __global__ void __launch_bounds__(XS_THREADS) tg_xsplit_kernel(const float* __re
   extern __shared__ float srow[];
   __shared__ float red[XS_THREADS / 32];
   grid_dep_launch();  // the MMA kernel may start its prologue (it waits before reading our output)
+  zero_split_counters(rscale, M_pad);
   const int64_t m = blockIdx.x;
   const float* grow = X + m * ldx;
   const bool in = m < M;
@@ -252,6 +264,7 @@ __global__ void __launch_bounds__(THREADS) tg_xsplit_reg_kernel(const float* __r
   __shared__ double red_d[NW];
   __shared__ int red_i[NW];
   grid_dep_launch();  // the MMA kernel may start its prologue (it waits before reading our output)
+  zero_split_counters(rscale, M_pad);
   if (threadIdx.x == 0) TG_GT(0);
   const int64_t m = blockIdx.x;
   const float* grow = X + m * ldx;
@@ -1253,7 +1266,9 @@ static int pick_splits(int64_t base_units, int64_t KC, int slots) {
   const int64_t smax = std::min<int64_t>(KC, 16);
   for (int64_t s = 1; s <= smax; ++s) {
     const int64_t rounds = ceil_div(base_units * s, slots);
-    const int64_t cost = rounds * (ceil_div(KC, s) + (s > 1 ? 2 : 0));
+    // a split unit pays its partial stores and the last arrival's reduction: measured on
+    // B200 at about 6 stages' worth (cfg2 / cfg4 with 2-4 splits: +4.5 to +13 us)
+    const int64_t cost = rounds * (ceil_div(KC, s) + (s > 1 ? 6 : 0));
     if (cost < best_cost) {
       best_cost = cost;
       best = int(s);
@@ -1343,10 +1358,13 @@ static SplitLayout split_layout(int64_t M, int64_t K, int64_t N, int share = 1) 
   L.NBG = ceil_div(L.NB, L.cs);
   L.clusters = N > 0 ? std::max(1, max_clusters_for(L.mt, L.cs) / std::max(1, share)) : 1;
   L.splits = N > 0 ? pick_splits(L.MB * L.NBG, ceil_div(L.KC, 2), L.clusters) : 1;
+  if (const char* env = getenv("TG_MMA_SPLITS"))  // experiments only
+    if (N > 0) L.splits = int(std::max<int64_t>(1, std::min<int64_t>(atoi(env), ceil_div(L.KC, 2))));
+  if (L.MB * L.NB > kSplitCounters) L.splits = 1;  // the split zeroes kSplitCounters counters
   L.off_rscale = size_t(round_up(3 * L.M_pad * L.K_pad, 256));
-  L.total_prepare = L.off_rscale + size_t(round_up(L.M_pad * int64_t(sizeof(double)), 256));
-  L.off_counters = L.total_prepare;
-  L.off_part = L.off_counters + size_t(round_up(L.MB * L.NB * 4, 256));
+  L.off_counters = L.off_rscale + size_t(round_up(L.M_pad * int64_t(sizeof(double)), 256));
+  L.total_prepare = L.off_counters + size_t(kSplitCounters) * 4;
+  L.off_part = L.total_prepare;
   L.total = L.splits > 1 ? L.off_part + size_t(L.splits) * 3 * size_t(L.M_pad) * size_t(L.N_pad) * 4
                          : L.total_prepare;
   return L;
@@ -1513,11 +1531,9 @@ int run_mma(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* t
     p.rank = sc->rank;
     p.col_off = sc->col_off;
   }
-  if (L.splits > 1) {
+  if (L.splits > 1) {  // (the counters were zeroed by the X split of this call)
     p.counters = reinterpret_cast<int32_t*>(base + L.off_counters);
     p.part = reinterpret_cast<int32_t*>(base + L.off_part);
-    cudaError_t e = cudaMemsetAsync(p.counters, 0, size_t(L.MB * L.NB) * 4, st);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaMemsetAsync(split counters)");
   }
   const int grid = int(std::min<int64_t>(p.units, L.clusters)) * L.cs;
   switch (L.mt * 10 + L.cs) {
