@@ -682,6 +682,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
       mbar_init(&tempty[a], C::EPI_WARPS);
     }
     fence_mbar_init();
+    *reinterpret_cast<unsigned long long*>(rs_s + 162) = 0ull;  // the CTA's PReLU count (epilogue)
     tma_prefetch_desc(&xmap);
     if (p.tma_y) tma_prefetch_desc(&ymap);
   }
@@ -1022,6 +1023,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
       if (p.tma_y && final_writer && !ghost) {
         fence_proxy_async_smem();  // our st.shared -> visible to the TMA (async proxy)
         named_bar_sync(1, ET);
+        if (et == 0 && lu == 0) TG_STAMP(7, 300);
         if (et == 0) {
           tma_store_2d(&ymap, ytile, n0, m0);
           bulk_commit_group();
@@ -1029,15 +1031,10 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
         if (p.sig_local) peer_copy_tile<MT>(p, ytile, m0, n0, et, ET);  // overlaps the local TMA store
       }
     }
-    // the smem tile must have been read before the CTA exits; the global writes complete
-    // with the grid (as CUTLASS's store tail).  The peer path keeps the full wait: its
-    // arrival signal below must follow this rank's own Y as well.
-    if (et == 0 && p.tma_y) {
-      if (p.sig_local) bulk_wait_group0();
-      else bulk_wait_group_read0();
-    }
     if (p.sig_local) {
-      // the last CTA to finish tells every rank that this rank's shard is in place
+      // the last CTA to finish tells every rank that this rank's shard is in place: its own
+      // Y (TMA store) must be complete too, not only read out of shared memory
+      if (et == 0 && p.tma_y) bulk_wait_group0();
       __threadfence_system();  // this thread's peer stores before the CTA's arrival
       named_bar_sync(1, ET);
       if (et == 0) {
@@ -1051,19 +1048,31 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
         }
       }
     }
+    if (et == 0) TG_STAMP(7, 301);
     if (et == 0) TG_STAMP(7, 3 + 2 * (lu - 1));
     if (et == 0) TG_GT(6);
     if (p.flags) {
+      // one global atomic per CTA: ~1000 same-address atomics from every warp of the grid
+      // serialise in L2 for microseconds at the end of the kernel
       if (__any_sync(0xffffffffu, any_bad) && lane == 0) atomicOr(&p.flags->nonfinite_output, 1);
       for (int o = 16; o; o >>= 1) npos += __shfl_xor_sync(0xffffffffu, npos, o);
-      if (lane == 0 && npos)
-        atomicAdd(reinterpret_cast<unsigned long long*>(&p.flags->nonpositive_outputs), npos);
+      unsigned long long* npos_s = reinterpret_cast<unsigned long long*>(rs_s + 162);
+      if (lane == 0 && npos) atomicAdd(npos_s, npos);
+      named_bar_sync(1, ET);
+      if (et == 0 && *npos_s) atomicAdd(reinterpret_cast<unsigned long long*>(&p.flags->nonpositive_outputs), *npos_s);
     }
+    // The smem Y tile must have been read by the TMA store before the CTA exits (waited for
+    // here, after the status words so the two overlap); the global writes complete with the
+    // grid, as in CUTLASS's store tail.
+    if (et == 0 && p.tma_y) bulk_wait_group_read0();
   }
+  if (threadIdx.x == 32 * C::EPI_WARP0) TG_STAMP(7, 302);
   __syncwarp();
   tc_fence_before();
   __syncthreads();
-  if (CS > 1) cluster_sync_all();  // no CTA leaves while peers may still multicast to it
+  if (threadIdx.x == 0) TG_STAMP(7, 303);
+  if (CS > 1) cluster_sync_relaxed();  // no CTA leaves while peers may still multicast to it
+  if (threadIdx.x == 0) TG_STAMP(7, 304);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<C::TMEM_COLS>(tmem_base);
