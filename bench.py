@@ -298,23 +298,35 @@ def run_ours(args) -> None:
     if assembly == "peer":
         from paper_2510_06957_b200.peer import PeerYBuffers, ScatterGemm
 
-        bufs = PeerYBuffers(M, N, symmetric=sym)
-        assert bufs.shard == sh, (bufs.shard, sh)
-        sg = ScatterGemm(lambda out, scatter: GemmRunner(kind, xin, fmt, db, method=method, alpha=wl.alpha, out=out,
-                                                         scatter=scatter), bufs)
-        for r in sg.runners:
-            r.pin_workspace()
-        # validate once: the kernel-assembled Y equals the NCCL-assembled Y bit for bit, on every slot
-        y_nccl = part.assemble(runner.y, y_full).clone()
-        ok = True
-        for _ in range(2 * bufs.slots):
-            yf = sg.step()
-            torch.cuda.synchronize()
-            ok = ok and bool(torch.equal(yf, y_nccl)) and not bufs.timed_out()
-        if max_over_ranks(0.0 if ok else 1.0, world, dev) != 0.0:
-            assembly, asm_note = "nccl", "peer scatter failed validation on some rank; fell back to NCCL all-gather"
+        # set-up failures (e.g. no cudaIpc between these processes) are agreed over the ranks
+        # and fall back to the NCCL all-gather instead of ending the run
+        why = None
+        try:
+            bufs = PeerYBuffers(M, N, symmetric=sym)
+            assert bufs.shard == sh, (bufs.shard, sh)
+            sg = ScatterGemm(lambda out, scatter: GemmRunner(kind, xin, fmt, db, method=method, alpha=wl.alpha,
+                                                             out=out, scatter=scatter), bufs)
+            for r in sg.runners:
+                r.pin_workspace()
+        except Exception as exc:  # noqa: BLE001 (reported in the JSON line)
+            why = f"{type(exc).__name__}: {exc}"
             sg = None
-        del y_nccl
+        if max_over_ranks(0.0 if why is None else 1.0, world, dev) != 0.0:
+            assembly = "nccl"
+            asm_note = f"peer buffers unavailable on some rank ({why or 'another rank'}); NCCL all-gather"
+            sg = bufs = None  # (left mapped: closing needs every rank)
+        else:
+            # validate once: the kernel-assembled Y equals the NCCL-assembled Y bit for bit, on every slot
+            y_nccl = part.assemble(runner.y, y_full).clone()
+            ok = True
+            for _ in range(2 * bufs.slots):
+                yf = sg.step()
+                torch.cuda.synchronize()
+                ok = ok and bool(torch.equal(yf, y_nccl)) and not bufs.timed_out()
+            if max_over_ranks(0.0 if ok else 1.0, world, dev) != 0.0:
+                assembly, asm_note = "nccl", "peer scatter failed validation on some rank; fell back to NCCL all-gather"
+                sg = None
+            del y_nccl
 
     def capture(fn):
         s = torch.cuda.Stream(device=dev)

@@ -411,8 +411,8 @@ struct HostGraph {
 constexpr int kHostGraphs = 16;
 
 #ifdef TG_TRACE
-// [chunk][0 = H2D done, 1 = GEMM done, 2 = D2H done] + the fork, recorded on direct enqueues
-cudaEvent_t g_host_ev[16][3];
+// [chunk][0 = H2D done, 1 = GEMM done, 2 = D2H done, 3 = X split done] + the fork, recorded on direct enqueues
+cudaEvent_t g_host_ev[16][4];
 cudaEvent_t g_host_ev0;
 int g_host_nev = 0;
 #define TG_HOST_EV(c, j, st)                                                                  \
@@ -472,6 +472,7 @@ int enqueue_host(const HostKey& k, const HostPlan& P, SideStreams* ss, cudaStrea
     void* wsi = static_cast<uint8_t*>(k.ws) + size_t(i) * P.ws_slice;
     if ((e = cudaStreamWaitEvent(st, ss->xin[c], 0)) != cudaSuccess) return set_cuda_error(e, "wait X chunk");
     TG_TRY(tg_gemm_tiles_prepare(xd, rows, K, k.ldx_dev, wsi, P.ws_slice, k.flags, st));
+    TG_HOST_EV(c, 3, st);
     TG_TRY(gemm_tiles_run(xd, rows, K, k.ldx_dev, k.tiles, N, k.bias, yd, k.ldy_dev, k.use_alpha, k.alpha, exact,
                           nullptr, wsi, P.ws_slice, k.flags, st, P.streams));
     if ((e = cudaEventRecord(ss->ydone[c], st)) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
@@ -524,11 +525,11 @@ cudaGraphExec_t capture_host(const HostKey& k, const HostPlan& P, SideStreams* s
 }  // namespace
 
 #ifdef TG_TRACE
-// ms since the fork of the last direct host-streaming call: out[3 c + j]; returns the chunk count
+// ms since the fork of the last direct host-streaming call: out[4 c + j]; returns the chunk count
 extern "C" int tg_debug_host_trace(float* out) {
   cudaDeviceSynchronize();
   for (int c = 0; c < g_host_nev; ++c)
-    for (int j = 0; j < 3; ++j) cudaEventElapsedTime(&out[3 * c + j], g_host_ev0, g_host_ev[c][j]);
+    for (int j = 0; j < 4; ++j) cudaEventElapsedTime(&out[4 * c + j], g_host_ev0, g_host_ev[c][j]);
   return g_host_nev;
 }
 #endif
