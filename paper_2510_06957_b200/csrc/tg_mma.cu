@@ -452,9 +452,13 @@ struct MmaCfg {
   static constexpr int STAGES_RAW = (TG_SMEM_BUDGET - 3072 - P_STAGES * P_BYTES - Y_BYTES) / B_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int ACC_COLS = (NMMA + 31) / 32 * 32;
-  static constexpr int A_SLOTS = 2;
   static constexpr int A_COLS = CH * 32;         // TMEM columns of one decoded stage
-  static constexpr int ACC_BUFS = (2 * ACC_COLS + A_SLOTS * A_COLS <= 512) ? 2 : 1;
+  static constexpr int ACC_BUFS = (2 * ACC_COLS + 2 * A_COLS <= 512) ? 2 : 1;
+  // decoded W^T slots: as many as TMEM holds next to the accumulators (at most 4, and no
+  // more than the X stages their release rides on), so the decoders can run stages ahead
+  static constexpr int A_SLOTS_ROOM = (512 - ACC_BUFS * ACC_COLS) / A_COLS;
+  static constexpr int A_SLOTS_MAX = A_SLOTS_ROOM < 4 ? A_SLOTS_ROOM : 4;
+  static constexpr int A_SLOTS = A_SLOTS_MAX < STAGES ? A_SLOTS_MAX : STAGES;
   static constexpr int A_BASE = ACC_BUFS * ACC_COLS;  // first TMEM column of the A ring
   static constexpr int TMEM_COLS = 512;
   static constexpr int SMEM =
@@ -700,18 +704,20 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
   if (threadIdx.x == 0) TG_GT(3);
 
   if (warp == 0) {
-    // ---------------- producer of the X limbs (TMA 2D, multicast to the cluster)
-    if (lane == 0) {
-      uint32_t it = 0;
-      for (int u = cid; u < p.units; u += ncl) {
-        int nb, mb, ks0, ks1, split;
-        unit_coords<CS>(p, u, crank, nb, mb, ks0, ks1, split);
-        const int m0 = mb * MT;
-        for (int ks = ks0; ks < ks1; ++ks, ++it) {
-          const int s = int(it % S);
-          const uint32_t r = it / S;
-          const int nch = (2 * ks + 1 < p.KC) ? 2 : 1;
-          mbar_wait(&empty[s], (r & 1) ^ 1);
+    // ---------------- producer of the X limbs (TMA 2D, multicast to the cluster).  The
+    // whole warp runs the loop and an elected lane issues (see the MMA issuer: an
+    // `if (lane == 0)` block costs a waterfall loop around every TMA instruction).
+    uint32_t it = 0;
+    for (int u = cid; u < p.units; u += ncl) {
+      int nb, mb, ks0, ks1, split;
+      unit_coords<CS>(p, u, crank, nb, mb, ks0, ks1, split);
+      const int m0 = mb * MT;
+      for (int ks = ks0; ks < ks1; ++ks, ++it) {
+        const int s = int(it % S);
+        const uint32_t r = it / S;
+        const int nch = (2 * ks + 1 < p.KC) ? 2 : 1;
+        mbar_wait(&empty[s], (r & 1) ^ 1);
+        if (elect_one()) {
           TG_STAMP(0, it);
           mbar_arrive_expect_tx(&full_raw[s], uint32_t(nch * C::B_CHUNK));
           for (int c = 0; c < nch; ++c) {
@@ -726,34 +732,45 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
             }
           }
         }
+        __syncwarp();
       }
     }
   } else if (warp == 6) {
     // ---------------- producer of the packed W tiles (own ring, runs ahead of the X ring)
-    if (lane == 0) {
-      uint32_t it = 0;
-      for (int u = cid; u < p.units; u += ncl) {
-        int nb, mb, ks0, ks1, split;
-        unit_coords<CS>(p, u, crank, nb, mb, ks0, ks1, split);
-        const int nsrc = nb < p.NB ? nb * C::BN : (p.NB - 1) * C::BN;  // ghost blocks decode a valid tile
-        for (int ks = ks0; ks < ks1; ++ks, ++it) {
-          const int sp = int(it % SP);
-          const uint32_t rp = it / SP;
-          const int nch = (2 * ks + 1 < p.KC) ? 2 : 1;
-          mbar_wait(&p_empty[sp], (rp & 1) ^ 1);
+    uint32_t it = 0;
+    for (int u = cid; u < p.units; u += ncl) {
+      int nb, mb, ks0, ks1, split;
+      unit_coords<CS>(p, u, crank, nb, mb, ks0, ks1, split);
+      const int nsrc = nb < p.NB ? nb * C::BN : (p.NB - 1) * C::BN;  // ghost blocks decode a valid tile
+      for (int ks = ks0; ks < ks1; ++ks, ++it) {
+        const int sp = int(it % SP);
+        const uint32_t rp = it / SP;
+        const int nch = (2 * ks + 1 < p.KC) ? 2 : 1;
+        mbar_wait(&p_empty[sp], (rp & 1) ^ 1);
+        if (elect_one()) {
           mbar_arrive_expect_tx(&p_full[sp], uint32_t(nch * C::P_CHUNK));
           for (int c = 0; c < nch; ++c)
             bulk_load(sP + sp * C::P_BYTES + c * C::P_CHUNK, p.tiles + (size_t(2 * ks + c) * p.N_pad + nsrc) * 8,
                       C::P_CHUNK, &p_full[sp]);
         }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer: A = decoded W^T from TMEM, B = X limbs from smem.
     // One commit per stage (to the stage's `empty` barrier, in every cluster CTA);
-    // the decoders derive the release of the A slot from the same barrier.
-    if (lane == 0) {
+    // the decoders derive the release of the A slot from the same barrier.  The whole
+    // warp runs the loop and one elected lane issues: inside an elect.sync block ptxas
+    // moves the operands to uniform registers directly, where an `if (lane == 0)` block
+    // got a waterfall loop (ELECT + R2UR.BROADCAST + branch) around every tcgen05.mma,
+    // ~70 cycles each -- the issue floor of small-N stages.
+    {
       constexpr uint32_t idesc = idesc_i8(128, C::NMMA);
+      // The CTA owns all 512 TMEM columns, so its allocation starts at address 0 (checked):
+      // compile-time operand addresses.
+      constexpr uint32_t tmem_base = 0;
+      static_assert(C::TMEM_COLS == 512, "the MMA issuer assumes the whole TMEM");
+      if (*tmem_slot != 0u) __trap();
       uint32_t it = 0, lu = 0;
       for (int u = cid; u < p.units; u += ncl, ++lu) {
         int nb, mb, ks0, ks1, split;
@@ -770,29 +787,33 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
           // a_full implies full_raw: the decoders arrive on a_full only after they
           // observed this stage's bytes land, and the MMA reads the X limbs through
           // the same async proxy that wrote them.
-          TG_STAMP(1, it);
+          if (lane == 0) TG_STAMP(1, it);
           mbar_wait(&a_full[a], ra & 1);
-          TG_STAMP(2, it);
+          if (lane == 0) TG_STAMP(2, it);
           tc_fence_after();
-          const uint64_t db = smem_desc_k_sw128(smem_u32(sB + s * C::B_BYTES));
-          const uint32_t ta = tmem_base + uint32_t(C::A_BASE + a * C::A_COLS);
-          for (int c = 0; c < nch; ++c) {
+          if (elect_one()) {
+            const uint64_t db = smem_desc_k_sw128(smem_u32(sB + s * C::B_BYTES));
+            const uint32_t ta = tmem_base + uint32_t(C::A_BASE + a * C::A_COLS);
+            for (int c = 0; c < nch; ++c) {
 #pragma unroll
-            for (int kk = 0; kk < C::BK / 32; ++kk) {
-              // K step of 32 int8: +8 TMEM columns for A, +32 bytes (= +2 in the >>4 field) for B
-              mma_i8_tmem_a(dtm, ta + uint32_t(c * 32 + kk * 8),
-                            db + uint64_t((c * C::B_CHUNK) >> 4) + uint64_t(kk * 2), idesc,
-                            (ks != ks0 || c != 0 || kk != 0) ? 1u : 0u);
+              for (int kk = 0; kk < C::BK / 32; ++kk) {
+                // K step of 32 int8: +8 TMEM columns for A, +32 bytes (= +2 in the >>4 field) for B
+                mma_i8_tmem_a(dtm, ta + uint32_t(c * 32 + kk * 8),
+                              db + uint64_t((c * C::B_CHUNK) >> 4) + uint64_t(kk * 2), idesc,
+                              (ks != ks0 || c != 0 || kk != 0) ? 1u : 0u);
+              }
             }
+            if (CS == 1) mma_commit(&empty[s]);
+            else mma_commit_mc(&empty[s], CMASK);
+            TG_STAMP(3, it);
+            if (it == 0) TG_GT(4);
           }
-          if (CS == 1) mma_commit(&empty[s]);
-          else mma_commit_mc(&empty[s], CMASK);
-          TG_STAMP(3, it);
-          if (it == 0) TG_GT(4);
+          __syncwarp();
         }
-        mma_commit(&tfull[acc]);
+        if (elect_one()) mma_commit(&tfull[acc]);
+        __syncwarp();
       }
-      TG_GT(5);
+      if (lane == 0) TG_GT(5);
     }
   } else if (warp < 6) {
     // ---------------- decoders (warps 2..5): packed smem -> decoded W^T rows in TMEM.
@@ -882,7 +903,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
       const bool n_ok = n < p.N;
       const float bf = (n_ok && p.bias) ? __ldg(p.bias + n) : 0.f;
       // previous unit: its TMA store must have read the Y tile, everyone done with the scales
-      if (et == 0 && p.tma_y) bulk_wait_group_read0();
+      if (et < 32 && p.tma_y && elect_one()) bulk_wait_group_read0();  // (the storing lane)
       named_bar_sync(1, ET);
       {  // stage the unit's row scales (and which rows are "wide") in shared memory
         const double rs = et < MT ? __ldcg(p.rscale + m0 + et) : 0.0;
@@ -1023,8 +1044,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
       if (p.tma_y && final_writer && !ghost) {
         fence_proxy_async_smem();  // our st.shared -> visible to the TMA (async proxy)
         named_bar_sync(1, ET);
-        if (et == 0 && lu == 0) TG_STAMP(7, 300);
-        if (et == 0) {
+        if (et < 32 && elect_one()) {  // (the same lane commits, and later waits for, the bulk group)
           tma_store_2d(&ymap, ytile, n0, m0);
           bulk_commit_group();
         }
@@ -1034,7 +1054,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
     if (p.sig_local) {
       // the last CTA to finish tells every rank that this rank's shard is in place: its own
       // Y (TMA store) must be complete too, not only read out of shared memory
-      if (et == 0 && p.tma_y) bulk_wait_group0();
+      if (et < 32 && p.tma_y && elect_one()) bulk_wait_group0();  // (the storing lane)
       __threadfence_system();  // this thread's peer stores before the CTA's arrival
       named_bar_sync(1, ET);
       if (et == 0) {
@@ -1064,7 +1084,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
     // The smem Y tile must have been read by the TMA store before the CTA exits (waited for
     // here, after the status words so the two overlap); the global writes complete with the
     // grid, as in CUTLASS's store tail.
-    if (et == 0 && p.tma_y) bulk_wait_group_read0();
+    if (et < 32 && p.tma_y && elect_one()) bulk_wait_group_read0();  // (the storing lane)
   }
   if (threadIdx.x == 32 * C::EPI_WARP0) TG_STAMP(7, 302);
   __syncwarp();
