@@ -465,7 +465,12 @@ struct MmaCfg {
       STAGES * B_BYTES + P_STAGES * P_BYTES + Y_BYTES + 1024 /*align*/ + 2048 /*barriers, scales*/;
   static constexpr int EPI_WARP0 = 7;            // warps: 0 X producer, 1 MMA, 2-5 decoders, 6 W producer
   static constexpr int EPI_WARPS = 8;            // two per TMEM lane quarter, splitting the rows
-  static constexpr int THREADS = 32 * (EPI_WARP0 + EPI_WARPS);
+  // Small MT: N <= 96 MMAs take ~60 cycles each, faster than one decoder group expands a
+  // stage (~700 cycles, mostly latency), so a second group (warps 15-18) takes every other
+  // stage.
+  static constexpr int DEC_GROUPS = MT <= 32 ? 2 : 1;
+  static constexpr int DEC2_WARP0 = EPI_WARP0 + EPI_WARPS;
+  static constexpr int THREADS = 32 * (EPI_WARP0 + EPI_WARPS + 4 * (DEC_GROUPS - 1));
   static_assert(MT % 16 == 0 && NMMA <= 256, "bad MT");
   static_assert(STAGES >= A_SLOTS, "slot release rides on the stage barrier: needs STAGES >= A_SLOTS");
   static_assert(STAGES >= 3 || MT < 64, "the X ring needs 3 stages at MT = 64");
@@ -700,7 +705,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
   // Programmatic dependent launch: everything above overlapped the X split.  Only
   // the X producer (limbs) and the epilogue (row scales) read its output and wait
   // for it; the W producer and the decoders start on the packed tiles at once.
-  if (warp == 0 || warp >= C::EPI_WARP0) grid_dep_wait();
+  if (warp == 0 || (warp >= C::EPI_WARP0 && warp < C::DEC2_WARP0)) grid_dep_wait();
   if (threadIdx.x == 0) TG_GT(3);
 
   if (warp == 0) {
@@ -815,10 +820,12 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
       }
       if (lane == 0) TG_GT(5);
     }
-  } else if (warp < 6) {
-    // ---------------- decoders (warps 2..5): packed smem -> decoded W^T rows in TMEM.
+  } else if (warp < 6 || warp >= C::DEC2_WARP0) {
+    // ---------------- decoders (warps 2..5, and 15..18 for the odd stages when
+    // DEC_GROUPS = 2): packed smem -> decoded W^T rows in TMEM.
     // Warp w may only access TMEM lanes 32*(w%4)..+31; lane = W^T row = output column.
     const int q = warp & 3;
+    const uint32_t grp = warp < 6 ? 0u : 1u;
     const uint32_t row = uint32_t(q * 32 + lane);
     const uint32_t lane_addr = uint32_t(q * 32) << 16;
     uint32_t it = 0;
@@ -826,6 +833,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
       int nb, mb, ks0, ks1, split;
       unit_coords<CS>(p, u, crank, nb, mb, ks0, ks1, split);
       for (int ks = ks0; ks < ks1; ++ks, ++it) {
+        if (it % C::DEC_GROUPS != grp) continue;  // the other group's stage
         const int s = int(it % S);
         const uint32_t r = it / S;
         const int a = int(it % AS);
