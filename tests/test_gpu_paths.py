@@ -206,3 +206,27 @@ def test_host_streaming_graph_replay(tg):
         tg.gemm_vectorized_optimal(tg.pad_input(Xpin), ibs, b, 0.25).values
     Xpin[100, 3] = 0.0
     assert np.isfinite(tg.gemm_vectorized_optimal(tg.pad_input(Xpin), ibs, b, 0.25).values).all()
+
+
+@pytest.mark.parametrize("chunks", ["8", "3", "1"])
+def test_host_streaming_multi_chunk(tg, chunks, monkeypatch):
+    """X large enough for several row chunks (ragged last one): in-order copy streams,
+    side-by-side chunk GEMMs on SM shares, graph replay of the whole pipeline; every
+    chunking gives the device-resident call's bits (wide rows included)."""
+    monkeypatch.setenv("TG_HOST_CHUNKS", chunks)
+    M, K, N = 1100, 2048, 640   # 9 MB of X: up to 4 chunks of 320 rows + 140
+    rng = np.random.default_rng(21)
+    W = rng.integers(-1, 2, size=(K, N)).astype(np.int8)
+    X = rng.standard_normal((M, K)).astype(np.float32)
+    X[700, 9] = 3e4  # a wide row inside the third chunk
+    b = rng.standard_normal(N).astype(np.float32)
+    Wd = torch.from_numpy(W).cuda()
+    ibs = tg.interleaved_blocked_from_dense(Wd, None, 2, True)
+    ref = tg.gemm_vectorized_optimal(tg.pad_input(torch.from_numpy(X).cuda()), ibs, b, 0.25).values.copy()
+    Xpin = torch.from_numpy(X).pin_memory()
+    for it in range(3):  # first call direct, second captured, third replayed
+        y = tg.gemm_vectorized_optimal(tg.pad_input(Xpin), ibs, b, 0.25)
+        assert np.array_equal(y.values, ref), (chunks, it)
+    t = tg.tcsc_from_dense(tg.TernaryDense(Wd))
+    ref_b = tg.gemm_base(torch.from_numpy(X).cuda(), t, b).values.copy()
+    assert np.array_equal(tg.gemm_base(X, t, b).values, ref_b)  # pageable numpy X
