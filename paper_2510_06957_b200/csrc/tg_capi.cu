@@ -178,7 +178,8 @@ int tg_gemm_tiles_prepare(const float* X, int64_t M, int64_t K, int64_t ldx, voi
 static int gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N,
                           const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha,
                           const tg_format_ref* exact, const tg_peer_scatter* sc, void* ws, size_t ws_bytes,
-                          tg_device_flags* flags, void* stream, int share = 1) {
+                          tg_device_flags* flags, void* stream, int share = 1, float* yh = nullptr,
+                          int64_t ldyh = 0) {
   TG_REQUIRE(M >= 1 && K >= 1 && N >= 1, TG_ERR_PARAM, "M, K and N must be >= 1");
   TG_REQUIRE(ldy >= N && ldx >= K, TG_ERR_PARAM, "leading dimensions too small");
   TG_REQUIRE(tiles && Y && ws && X, TG_ERR_PARAM, "null pointer");
@@ -195,7 +196,7 @@ static int gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, con
   TG_REQUIRE(ws_bytes >= mma_ws_bytes(M, K, N, share), TG_ERR_PARAM, "workspace too small");
   TG_TRY(require_device());
   if (!exact) return run_mma(X, M, K, ldx, tiles, N, bias, Y, ldy, use_alpha, alpha, nullptr, ws, ws_bytes, flags,
-                             as_stream(stream), sc, share);
+                             as_stream(stream), sc, share, yh, ldyh);
   const int v = exact->variant;
   MmaFixup fx{};
   const int64_t nb = (v == TG_VARIANT_BASE || v == TG_VARIANT_UNROLLED) ? 1 : ceil_div(K, exact->B);
@@ -215,7 +216,7 @@ static int gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, con
                          v == TG_VARIANT_BASE ? 1 : exact->uf, nullptr, 0};
   }
   return run_mma(X, M, K, ldx, tiles, N, bias, Y, ldy, use_alpha, alpha, &fx, ws, ws_bytes, flags,
-                 as_stream(stream), sc, share);
+                 as_stream(stream), sc, share, yh, ldyh);
 }
 
 int tg_gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N,
@@ -452,6 +453,20 @@ int enqueue_host(const HostKey& k, const HostPlan& P, SideStreams* ss, cudaStrea
     return set_cuda_error(e, "fork");
   const tg_format_ref* exact = k.has_exact ? &k.exact : nullptr;
   const int64_t M = k.M, K = k.K, N = k.N;
+  // Y straight from the epilogue into the pinned host Y when it is device-mapped and
+  // 16-byte aligned (no copy-engine D2H: those transfers delay the launches of the
+  // chunks' kernels that run beside them); TG_HOST_ZEROCOPY=0 keeps the copies
+  float* yh = nullptr;
+  static const bool zc_on = [] {
+    const char* env = getenv("TG_HOST_ZEROCOPY");
+    return !(env && env[0] == '0');
+  }();
+  if (zc_on && (reinterpret_cast<uintptr_t>(k.Y_host) & 15) == 0 && (k.ldy_host * 4) % 16 == 0) {
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, k.Y_host) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+      yh = static_cast<float*>(pa.devicePointer);
+    cudaGetLastError();
+  }
   for (int64_t c = 0; c < P.n; ++c) {  // X chunks in, in order
     const int64_t r0 = c * P.rows, rows = std::min(P.rows, M - r0);
     float* xd = k.X_dev + r0 * k.ldx_dev;
@@ -474,7 +489,8 @@ int enqueue_host(const HostKey& k, const HostPlan& P, SideStreams* ss, cudaStrea
     TG_TRY(tg_gemm_tiles_prepare(xd, rows, K, k.ldx_dev, wsi, P.ws_slice, k.flags, st));
     TG_HOST_EV(c, 3, st);
     TG_TRY(gemm_tiles_run(xd, rows, K, k.ldx_dev, k.tiles, N, k.bias, yd, k.ldy_dev, k.use_alpha, k.alpha, exact,
-                          nullptr, wsi, P.ws_slice, k.flags, st, P.streams));
+                          nullptr, wsi, P.ws_slice, k.flags, st, P.streams, yh ? yh + r0 * k.ldy_host : nullptr,
+                          k.ldy_host));
     if ((e = cudaEventRecord(ss->ydone[c], st)) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
     TG_HOST_EV(c, 1, st);
   }
@@ -482,6 +498,10 @@ int enqueue_host(const HostKey& k, const HostPlan& P, SideStreams* ss, cudaStrea
     const int64_t r0 = c * P.rows, rows = std::min(P.rows, M - r0);
     const float* yd = k.Y_dev + r0 * k.ldy_dev;
     if ((e = cudaStreamWaitEvent(ss->cout, ss->ydone[c], 0)) != cudaSuccess) return set_cuda_error(e, "wait Y");
+    if (yh) {  // already in host memory
+      TG_HOST_EV(c, 2, ss->cout);
+      continue;
+    }
     e = k.ldy_dev == N && k.ldy_host == N
             ? cudaMemcpyAsync(k.Y_host + r0 * N, yd, size_t(rows * N) * 4, cudaMemcpyDeviceToHost, ss->cout)
             : cudaMemcpy2DAsync(k.Y_host + r0 * k.ldy_host, size_t(k.ldy_host) * 4, yd, size_t(k.ldy_dev) * 4,

@@ -63,5 +63,6 @@ int run_pack_sym(const int32_t* idx, const int32_t* ptr, int64_t N, int g, int64
 int run_pack_codes(const uint8_t* codes, int64_t K, int64_t N, uint32_t* tiles, cudaStream_t st);
 int run_mma(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N, const float* bias,
             float* Y, int64_t ldy, int use_alpha, float alpha, const MmaFixup* fix, void* ws, size_t ws_bytes,
-            tg_device_flags* flags, cudaStream_t st, const tg_peer_scatter* sc = nullptr, int share = 1);
+            tg_device_flags* flags, cudaStream_t st, const tg_peer_scatter* sc = nullptr, int share = 1,
+            float* yh = nullptr, int64_t ldyh = 0);
 }  // namespace tg

@@ -413,6 +413,10 @@ struct MmaParams {
   uint32_t* sig_local;
   int world, rank;
   int64_t col_off;
+  // host streaming: every finished tile is also stored straight into the caller's pinned
+  // host Y (device-mapped), so no copy-engine D2H follows the GEMM; null: off
+  float* yh;
+  int64_t ldyh;
 };
 
 // One Y row segment to every other rank's full Y (plain st.global over NVLink).
@@ -512,6 +516,7 @@ struct EmitCtx {
   float* ydst;       // false: Y (row stride ldy)
   int64_t ystride;
   int64_t yoff;      // element offset of ydst in this rank's full Y (peer scatter)
+  int n;             // output column (host Y copy of direct stores)
 };
 
 __device__ __forceinline__ void load_scales(uint32_t addr, float4 (&sc)[16]) {
@@ -584,6 +589,12 @@ __device__ __forceinline__ void emit_tail(float (&v)[16], const uint32_t* r0, co
     for (int j = 0; j < 16; ++j)
       if (j < e.nvalid) e.ydst[int64_t(j) * e.ystride] = v[j];
   }
+  if (p.yh) {
+    float* d = p.yh + int64_t(e.m_first) * p.ldyh + e.n;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < e.nvalid) d[int64_t(j) * p.ldyh] = v[j];
+  }
   if (p.sig_local) {
 #pragma unroll 1
     for (int q = 0; q < p.world; ++q) {
@@ -619,6 +630,27 @@ __device__ __forceinline__ void peer_copy_tile(const MmaParams& p, const float* 
         if (c + 1 < cols) d[1] = v.y;
         if (c + 2 < cols) d[2] = v.z;
       }
+    }
+  }
+}
+
+// A finished smem Y tile to the pinned host Y (16-byte stores over PCIe).
+template <int MT>
+__device__ __forceinline__ void host_copy_tile(const MmaParams& p, const float* ytile, int m0, int n0, int et,
+                                               int nthreads) {
+  const int rows = min(MT, p.M - m0), cols = min(128, p.N - n0);
+#pragma unroll 1
+  for (int i = et; i < rows * 32; i += nthreads) {
+    const int r = i >> 5, c = (i & 31) * 4;
+    if (c >= cols) continue;
+    const float4 v = *reinterpret_cast<const float4*>(ytile + r * 128 + c);
+    float* d = p.yh + int64_t(m0 + r) * p.ldyh + n0 + c;
+    if (c + 4 <= cols) {
+      *reinterpret_cast<float4*>(d) = v;
+    } else {
+      d[0] = v.x;
+      if (c + 1 < cols) d[1] = v.y;
+      if (c + 2 < cols) d[2] = v.z;
     }
   }
 }
@@ -943,6 +975,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
         e.ydst = p.Y + int64_t(m0 + mm) * p.ldy + n;
         e.ystride = p.ldy;
         e.yoff = p.col_off + int64_t(m0 + mm) * p.ldy + n;
+        e.n = n;
         return e;
       };
 #pragma unroll 1
@@ -1044,6 +1077,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
               ytile[j * C::BN + c] = y;
             } else {
               p.Y[int64_t(m) * p.ldy + n] = y;
+              if (p.yh) p.yh[int64_t(m) * p.ldyh + n] = y;
               if (p.sig_local) peer_store(p, p.col_off + int64_t(m) * p.ldy + n, y);
             }
           }
@@ -1057,6 +1091,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
           bulk_commit_group();
         }
         if (p.sig_local) peer_copy_tile<MT>(p, ytile, m0, n0, et, ET);  // overlaps the local TMA store
+        if (p.yh) host_copy_tile<MT>(p, ytile, m0, n0, et, ET);
       }
     }
     if (p.sig_local) {
@@ -1496,7 +1531,8 @@ static int launch_mma(const CUtensorMap& map, const CUtensorMap& ymap, const Mma
 
 int run_mma(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N, const float* bias,
             float* Y, int64_t ldy, int use_alpha, float alpha, const MmaFixup* fix, void* ws, size_t ws_bytes,
-            tg_device_flags* flags, cudaStream_t st, const tg_peer_scatter* sc, int share) {
+            tg_device_flags* flags, cudaStream_t st, const tg_peer_scatter* sc, int share, float* yh,
+            int64_t ldyh) {
   const SplitLayout L = split_layout(M, K, N, share);
   if (ws_bytes < L.total) return set_error(TG_ERR_PARAM, "workspace too small for the tensor-core path");
   uint8_t* base = static_cast<uint8_t*>(ws);
@@ -1560,6 +1596,8 @@ int run_mma(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* t
     p.X = X;
     p.ldx = ldx;
   }
+  p.yh = yh;
+  p.ldyh = ldyh;
   if (sc) {
     p.ypeers = sc->y_peers;
     p.speers = sc->sig_peers;
