@@ -504,7 +504,7 @@ __device__ __forceinline__ void unit_coords(const MmaParams& p, int u, int crank
 //   scale leaves the float range are "wide" and recomputed exactly afterwards
 //   (or, without an exact-order format, here in full-range fp64).
 struct EmitCtx {
-  uint32_t sc_addr;  // smem address of the float4 scales of row m_first
+  uint32_t sc_addr;  // smem address of the float scale of row m_first
   float bf;
   uint32_t wide_bits;
   int m_first;
@@ -519,12 +519,24 @@ struct EmitCtx {
   int n;             // output column (host Y copy of direct stores)
 };
 
+// Row scales of 16 consecutive rows.  Full form: {2^-s, 2^(8-s), 2^(16-s), 2^(24-s)} per row
+// (one ld.shared.v4 each).  Compact form (the 608-thread small-tile kernels, whose register
+// budget is 104): 2^-s only; 2^(8-s) and 2^(16-s) are exact power-of-two multiples of it for
+// every row whose scale is in range (the others are "wide" and recomputed).  Measured: the
+// full form is ~4% faster at MT = 64, the compact one avoids spills at MT <= 32 (cfg4 -2 us).
 __device__ __forceinline__ void load_scales(uint32_t addr, float4 (&sc)[16]) {
 #pragma unroll
   for (int j = 0; j < 16; ++j)
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                  : "=f"(sc[j].x), "=f"(sc[j].y), "=f"(sc[j].z), "=f"(sc[j].w)
                  : "r"(addr + 16u * j));
+}
+__device__ __forceinline__ void load_scales(uint32_t addr, float (&sc)[16]) {
+#pragma unroll
+  for (int j = 0; j < 16; j += 4)
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(sc[j]), "=f"(sc[j + 1]), "=f"(sc[j + 2]), "=f"(sc[j + 3])
+                 : "r"(addr + 4u * j));
 }
 
 // tail shared by both emitters: PReLU, PReLU count, finiteness, the rare fp64 rows, store
@@ -656,16 +668,28 @@ __device__ __forceinline__ void host_copy_tile(const MmaParams& p, const float* 
 }
 
 // from the three limb sums of a finished accumulator (TMEM)
+template <bool COMPACT>
 __device__ __forceinline__ void emit16_limbs(const uint32_t (&r0)[16], const uint32_t (&r1)[16],
                                              const uint32_t (&r2)[16], const EmitCtx& e, const MmaParams& p,
                                              unsigned long long& npos, bool& bad) {
-  float4 sc[16];
-  load_scales(e.sc_addr, sc);
   float v[16];
+  if constexpr (COMPACT) {
+    float sc[16];
+    load_scales(e.sc_addr, sc);
 #pragma unroll
-  for (int j = 0; j < 16; ++j)
-    v[j] = __fmaf_rn(float(int(r0[j])), sc[j].z,
-                     __fmaf_rn(float(int(r1[j])), sc[j].y, __fmaf_rn(float(int(r2[j])), sc[j].x, e.bf)));
+    for (int j = 0; j < 16; ++j) {
+      const float s0 = sc[j], s1 = s0 * 256.f, s2 = s0 * 65536.f;
+      v[j] = __fmaf_rn(float(int(r0[j])), s2,
+                       __fmaf_rn(float(int(r1[j])), s1, __fmaf_rn(float(int(r2[j])), s0, e.bf)));
+    }
+  } else {
+    float4 sc[16];
+    load_scales(e.sc_addr, sc);
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      v[j] = __fmaf_rn(float(int(r0[j])), sc[j].z,
+                       __fmaf_rn(float(int(r1[j])), sc[j].y, __fmaf_rn(float(int(r2[j])), sc[j].x, e.bf)));
+  }
   emit_tail(v, r0, r1, r2, e, p, npos, bad);
 }
 
@@ -697,8 +721,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
   uint64_t* tempty = tfull + 2;             // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int32_t* last_flag = reinterpret_cast<int32_t*>(tmem_slot + 1);
-  // [80] float4 row scales {2^-s, 2^(8-s), 2^(16-s), 2^(24-s)} of the current unit (16-byte
-  // aligned), then [4] wide-row masks
+  // [80] row scales of the current unit (float or float4 each, 16-byte aligned), then [4] wide-row masks
   double* rs_s = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(tmem_slot + 2) + 15) & ~uintptr_t(15));
 
   const int warp = threadIdx.x >> 5;
@@ -927,7 +950,8 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
     const int et = threadIdx.x - 32 * C::EPI_WARP0;  // 0..ET-1
     const int half = (warp - C::EPI_WARP0) >> 2;
     const uint32_t rs_addr = smem_u32(rs_s);
-    float4* sc_s = reinterpret_cast<float4*>(rs_s);
+    constexpr bool COMPACT = C::DEC_GROUPS > 1;     // (the 608-thread kernels: see load_scales)
+    float* sc_s = reinterpret_cast<float*>(rs_s);  // [80] row scales of the unit (x4 when !COMPACT)
     uint32_t* wmask = reinterpret_cast<uint32_t*>(rs_s + 160);  // [4] wide-row bits of the unit (after 80 float4)
     bool any_bad = false;
     unsigned long long npos = 0;
@@ -949,7 +973,9 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
         const double rs = et < MT ? __ldcg(p.rscale + m0 + et) : 0.0;
         if (et < MT) {
           const double a = fabs(rs);
-          sc_s[et] = make_float4(float(a), float(a * 256.0), float(a * 65536.0), float(a * 16777216.0));
+          if (COMPACT) sc_s[et] = float(a);
+          else reinterpret_cast<float4*>(sc_s)[et] =
+              make_float4(float(a), float(a * 256.0), float(a * 65536.0), float(a * 16777216.0));
         }
         const uint32_t wbits = __ballot_sync(0xffffffffu, rs < 0.0);
         if (lane == 0 && (et >> 5) < 4) wmask[et >> 5] = wbits;
@@ -962,7 +988,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
       bool final_writer = p.splits == 1;
       auto ctx = [&](int mm) {
         EmitCtx e;
-        e.sc_addr = rs_addr + 16u * uint32_t(mm);
+        e.sc_addr = rs_addr + (COMPACT ? 4u : 16u) * uint32_t(mm);
         e.bf = bf;
         e.wide_bits = (wmask[mm >> 5] >> (mm & 31)) & 0xFFFFu;
         e.m_first = m0 + mm;
@@ -993,7 +1019,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
 #endif
         if (et == 0 && lu == 0) TG_STAMP(7, 220 + mm / 16);
         if (p.splits == 1) {
-          emit16_limbs(r0, r1, r2, ctx(mm), p, npos, any_bad);
+          emit16_limbs<COMPACT>(r0, r1, r2, ctx(mm), p, npos, any_bad);
           if (et == 0 && lu == 0) TG_STAMP(7, 240 + mm / 16);
         } else if (!ghost) {
           // per-limb partials: the reduced sums take exactly the unsplit epilogue, so a
@@ -1051,7 +1077,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
                 t2[j] += uint32_t(__ldcg(s2 + 2 * plane + int64_t(j) * p.N_pad));
               }
             }
-            emit16_limbs(t0, t1, t2, ctx(j0), p, npos, any_bad);
+            emit16_limbs<COMPACT>(t0, t1, t2, ctx(j0), p, npos, any_bad);
           }
         }
         named_bar_sync(1, ET);  // last_flag is reused by the next unit
