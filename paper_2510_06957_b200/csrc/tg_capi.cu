@@ -467,7 +467,20 @@ int enqueue_host(const HostKey& k, const HostPlan& P, SideStreams* ss, cudaStrea
       yh = static_cast<float*>(pa.devicePointer);
     cudaGetLastError();
   }
-  for (int64_t c = 0; c < P.n; ++c) {  // X chunks in, in order
+  // X read straight from the pinned host X by the split kernels (TG_HOST_ZEROCOPY_X=1):
+  // no copy engine at all in the pipeline
+  const float* xh = nullptr;
+  static const bool zcx_on = [] {
+    const char* env = getenv("TG_HOST_ZEROCOPY_X");
+    return env && env[0] == '1';
+  }();
+  if (zcx_on) {
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, k.X_host) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+      xh = static_cast<const float*>(pa.devicePointer);
+    cudaGetLastError();
+  }
+  for (int64_t c = 0; c < P.n && !xh; ++c) {  // X chunks in, in order
     const int64_t r0 = c * P.rows, rows = std::min(P.rows, M - r0);
     float* xd = k.X_dev + r0 * k.ldx_dev;
     e = k.ldx_dev == K && k.ldx_host == K
@@ -482,13 +495,14 @@ int enqueue_host(const HostKey& k, const HostPlan& P, SideStreams* ss, cudaStrea
     const int i = int(c % P.streams);
     cudaStream_t st = ss->s[i];
     const int64_t r0 = c * P.rows, rows = std::min(P.rows, M - r0);
-    float* xd = k.X_dev + r0 * k.ldx_dev;
+    const float* xd = xh ? xh + r0 * k.ldx_host : k.X_dev + r0 * k.ldx_dev;
+    const int64_t ldx = xh ? k.ldx_host : k.ldx_dev;
     float* yd = k.Y_dev + r0 * k.ldy_dev;
     void* wsi = static_cast<uint8_t*>(k.ws) + size_t(i) * P.ws_slice;
-    if ((e = cudaStreamWaitEvent(st, ss->xin[c], 0)) != cudaSuccess) return set_cuda_error(e, "wait X chunk");
-    TG_TRY(tg_gemm_tiles_prepare(xd, rows, K, k.ldx_dev, wsi, P.ws_slice, k.flags, st));
+    if (!xh && (e = cudaStreamWaitEvent(st, ss->xin[c], 0)) != cudaSuccess) return set_cuda_error(e, "wait X chunk");
+    TG_TRY(tg_gemm_tiles_prepare(xd, rows, K, ldx, wsi, P.ws_slice, k.flags, st));
     TG_HOST_EV(c, 3, st);
-    TG_TRY(gemm_tiles_run(xd, rows, K, k.ldx_dev, k.tiles, N, k.bias, yd, k.ldy_dev, k.use_alpha, k.alpha, exact,
+    TG_TRY(gemm_tiles_run(xd, rows, K, ldx, k.tiles, N, k.bias, yd, k.ldy_dev, k.use_alpha, k.alpha, exact,
                           nullptr, wsi, P.ws_slice, k.flags, st, P.streams, yh ? yh + r0 * k.ldy_host : nullptr,
                           k.ldy_host));
     if ((e = cudaEventRecord(ss->ydone[c], st)) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
