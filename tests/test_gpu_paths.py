@@ -230,3 +230,47 @@ def test_host_streaming_multi_chunk(tg, chunks, monkeypatch):
     t = tg.tcsc_from_dense(tg.TernaryDense(Wd))
     ref_b = tg.gemm_base(torch.from_numpy(X).cuda(), t, b).values.copy()
     assert np.array_equal(tg.gemm_base(X, t, b).values, ref_b)  # pageable numpy X
+
+
+@pytest.mark.parametrize("zerocopy_pitch", [False, True])
+def test_host_streaming_c_abi_pitched(tg, zerocopy_pitch):
+    """tg_gemm_tiles_host through the C ABI with pitched buffers: host X of pitch K+1
+    (2-D copies), a padded device staging X (ldx_dev > K: its slot columns are zeroed),
+    a device Y of pitch N+3, and a host Y whose pitch either rules out the zero-copy
+    store (N+1: 2-D D2H copies) or allows it (N+4).  Y and the status words must equal the
+    device-resident call."""
+    import ctypes
+
+    from paper_2510_06957_b200 import _native as nat
+
+    M, K, N = 600, 1536, 256
+    rng = np.random.default_rng(33)
+    W = rng.integers(-1, 2, size=(K, N)).astype(np.int8)
+    X = rng.standard_normal((M, K)).astype(np.float32)
+    b = rng.standard_normal(N).astype(np.float32)
+    Wd = torch.from_numpy(W).cuda()
+    t = tg.tcsc_from_dense(tg.TernaryDense(Wd))
+    ref = tg.gemm_base(torch.from_numpy(X).cuda(), t, b).values
+    L = nat.load()
+    hx = torch.zeros((M, K + 1)).pin_memory()
+    hx[:, :K] = torch.from_numpy(X)
+    xd = torch.full((M, K + 5), 7.0, device="cuda")       # slot columns must be zeroed by the call
+    yd = torch.empty((M, N + 3), device="cuda")
+    ldyh = N + 4 if zerocopy_pitch else N + 1
+    yh = torch.full((M, ldyh), -1.0).pin_memory()
+    fl = torch.zeros(6, dtype=torch.int32, device="cuda")
+    fh = torch.full((6,), 99, dtype=torch.int32).pin_memory()
+    ws = torch.empty(L.tg_gemm_host_workspace_bytes(M, K, N), dtype=torch.uint8, device="cuda")
+    bd = torch.from_numpy(b).cuda()
+    r = tg.kernels.GemmRunner("base", xd, t, bd, method="mma")
+    for _ in range(3):  # direct, captured, replayed
+        nat.call("tg_gemm_tiles_host", ctypes.c_void_p(hx.data_ptr()), M, K, K + 1, ctypes.c_void_p(xd.data_ptr()),
+                 K + 5, ctypes.c_void_p(t.tiles().data_ptr()), N, ctypes.c_void_p(bd.data_ptr()),
+                 ctypes.c_void_p(yd.data_ptr()), N + 3, ctypes.c_void_p(yh.data_ptr()), ldyh, 0, 0.0,
+                 ctypes.byref(r.exact), ctypes.c_void_p(ws.data_ptr()), ws.numel(), ctypes.c_void_p(fl.data_ptr()),
+                 ctypes.c_void_p(fh.data_ptr()), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(yh.numpy()[:, :N], ref)
+        assert torch.equal(yd[:, :N].cpu(), torch.from_numpy(ref))
+        assert bool((xd[:, K:] == 0).all())
+        assert int(fh[0]) == 0 and int(fh[1]) == 0
