@@ -79,10 +79,15 @@ __device__ __forceinline__ unsigned long long gtime() {
 // Row m is scaled by 2^s, s = 22 - e with amax < 2^e, so |x 2^s| < 2^22; the
 // rounded integer v splits into balanced base-256 digits v = d0 2^16 + d1 2^8 + d2.
 // The grid step 2^(e-22) is relative to the row maximum, so a row whose nonzero
-// entries span a wide dynamic range (amax > kWideRatio * rms of its nonzeros)
-// gets its rscale stored negated: the MMA epilogue then recomputes the row in
-// the exact reference order (and takes its PReLU count there).
+// entries span a wide dynamic range gets its rscale stored negated: the MMA
+// epilogue then recomputes the row in the exact reference order (and takes its
+// PReLU count there).  Wide means amax > kWideRatio * rms of its nonzeros, or
+// fewer than 1/kWideFrac of its nonzeros within kWideRatio of amax.  The second
+// rule catches a few outliers in a short row (one entry 5000x the rest in K = 128
+// passes the rms test, yet leaves the other entries 9 bits on the grid: an output
+// that does not see the outlier then misses the 1e-5 bar; tests/test_gpu_fuzz.py).
 constexpr float kWideRatio = 16.f;
+constexpr int kWideFrac = 4;
 // The epilogue applies 2^-s and 2^(24-s) as normal floats: |s| <= 100 keeps both
 // (and every partial product) far inside the fp32 range.  Rows outside take the
 // exact-order path.
@@ -200,7 +205,7 @@ __global__ void __launch_bounds__(XS_THREADS) tg_xsplit_kernel(const float* __re
   const int s_a = s > 126 ? 126 : (s < -126 ? -126 : s);
   const float sc_a = __int_as_float((127 + s_a) << 23), sc_b = __int_as_float((127 + s - s_a) << 23);
   const float inv = live ? 1.f / amax : 0.f;
-  float s2 = 0.f, nzf = 0.f;
+  float s2 = 0.f, nzf = 0.f, bigf = 0.f;
   int8_t* l0 = limbs + m * K_pad;
   int8_t* l1 = limbs + (M_pad + m) * K_pad;
   int8_t* l2 = limbs + (2 * M_pad + m) * K_pad;
@@ -221,6 +226,7 @@ __global__ void __launch_bounds__(XS_THREADS) tg_xsplit_kernel(const float* __re
           const float t = x * inv;
           s2 += t * t;
           nzf += (x != 0.f) ? 1.f : 0.f;
+          bigf += (fabsf(t) * kWideRatio >= 1.f) ? 1.f : 0.f;
         }
         p0 |= limb_digits(v, p1, p2, j);
       }
@@ -240,9 +246,12 @@ __global__ void __launch_bounds__(XS_THREADS) tg_xsplit_kernel(const float* __re
   }
   s2 = block_sum<XS_THREADS>(s2, red);
   nzf = block_sum<XS_THREADS>(nzf, red);
+  bigf = block_sum<XS_THREADS>(bigf, red);
   if (threadIdx.x == 0) {
-    // amax / rms(nonzeros) > kWideRatio, or a scale outside the epilogue's fp32 range
-    const bool is_wide = live && (nzf > kWideRatio * kWideRatio * s2 || s > kMaxScaleExp || s < -kMaxScaleExp);
+    // amax / rms(nonzeros) > kWideRatio, few entries near amax, or a scale outside the
+    // epilogue's fp32 range
+    const bool is_wide = live && (nzf > kWideRatio * kWideRatio * s2 || bigf * kWideFrac < nzf ||
+                                  s > kMaxScaleExp || s < -kMaxScaleExp);
     const double sc = live ? ldexp(1.0, -s) : 0.0;
     rscale[m] = is_wide ? -sc : sc;
   }
@@ -263,6 +272,7 @@ __global__ void __launch_bounds__(THREADS) tg_xsplit_reg_kernel(const float* __r
   __shared__ float red_f[NW];
   __shared__ double red_d[NW];
   __shared__ int red_i[NW];
+  __shared__ int red_b[2];
   grid_dep_launch();  // the MMA kernel may start its prologue (it waits before reading our output)
   zero_split_counters(rscale, M_pad);
   if (threadIdx.x == 0) TG_GT(0);
@@ -301,6 +311,7 @@ __global__ void __launch_bounds__(THREADS) tg_xsplit_reg_kernel(const float* __r
     red_d[w] = s2;
     red_i[w] = nz;
   }
+  if (threadIdx.x == 0) red_b[0] = red_b[1] = 0;  // the big-entry count and the warp arrivals
   __syncthreads();
   amax = red_f[0];
   s2 = red_d[0];
@@ -321,48 +332,61 @@ __global__ void __launch_bounds__(THREADS) tg_xsplit_reg_kernel(const float* __r
   } else if (in && !finite && threadIdx.x == 0 && flags) {
     atomicOr(&flags->bad_input, 4);
   }
-  if (threadIdx.x == 0) {
-    // amax / rms(nonzeros) > kWideRatio  <=>  nz * amax^2 > kWideRatio^2 * sum x^2
-    const bool is_wide = live && (double(nz) * double(amax) * double(amax) > double(kWideRatio * kWideRatio) * s2 ||
-                                  s > kMaxScaleExp || s < -kMaxScaleExp);
-    const double sc = live ? ldexp(1.0, -s) : 0.0;
-    rscale[m] = is_wide ? -sc : sc;
-    TG_GT(1);
-  }
-  if (k0 >= K_pad) return;
-  // x * 2^s as two exact power-of-two multiplies (2^s alone may exceed the float range)
-  const int s_a = s > 126 ? 126 : (s < -126 ? -126 : s);
-  const float sc_a = __int_as_float((127 + s_a) << 23), sc_b = __int_as_float((127 + s - s_a) << 23);
-  uint32_t w0[EPT / 4], w1[EPT / 4], w2[EPT / 4];
+  // Entries within kWideRatio of amax: counted after the limbs are stored (no second
+  // barrier before the stores): each warp adds its count, the last warp to arrive writes
+  // the row's scale and wide flag.
+  int big = 0;
 #pragma unroll
-  for (int j = 0; j < EPT; j += 4) {
-    uint32_t u[4];
+  for (int j = 0; j < EPT; ++j) big += (fabsf(x[j]) * kWideRatio >= amax && x[j] != 0.f) ? 1 : 0;
+  if (k0 < K_pad) {
+    // x * 2^s as two exact power-of-two multiplies (2^s alone may exceed the float range)
+    const int s_a = s > 126 ? 126 : (s < -126 ? -126 : s);
+    const float sc_a = __int_as_float((127 + s_a) << 23), sc_b = __int_as_float((127 + s - s_a) << 23);
+    uint32_t w0[EPT / 4], w1[EPT / 4], w2[EPT / 4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) u[i] = uint32_t((live ? __float2int_rn((x[j + i] * sc_a) * sc_b) : 0) + 0x808080);
-    const uint32_t lo01 = __byte_perm(u[0], u[1], 0x5140);  // b0(u0) b0(u1) b1(u0) b1(u1)
-    const uint32_t lo23 = __byte_perm(u[2], u[3], 0x5140);
-    const uint32_t hi01 = __byte_perm(u[0], u[1], 0x7362);  // b2(u0) b2(u1) b3 b3
-    const uint32_t hi23 = __byte_perm(u[2], u[3], 0x7362);
-    w2[j / 4] = __byte_perm(lo01, lo23, 0x5410) ^ 0x80808080u;  // byte 0 of each u: low digit
-    w1[j / 4] = __byte_perm(lo01, lo23, 0x7632) ^ 0x80808080u;  // byte 1: middle digit
-    w0[j / 4] = __byte_perm(hi01, hi23, 0x5410) ^ 0x80808080u;  // byte 2: high digit
-  }
-  int8_t* l0 = limbs + m * K_pad + k0;
-  int8_t* l1 = limbs + (M_pad + m) * K_pad + k0;
-  int8_t* l2 = limbs + (2 * M_pad + m) * K_pad + k0;
-  if constexpr (EPT % 16 == 0) {
+    for (int j = 0; j < EPT; j += 4) {
+      uint32_t u[4];
 #pragma unroll
-    for (int j = 0; j < EPT / 4; j += 4) {
-      reinterpret_cast<uint4*>(l0)[j / 4] = make_uint4(w0[j], w0[j + 1], w0[j + 2], w0[j + 3]);
-      reinterpret_cast<uint4*>(l1)[j / 4] = make_uint4(w1[j], w1[j + 1], w1[j + 2], w1[j + 3]);
-      reinterpret_cast<uint4*>(l2)[j / 4] = make_uint4(w2[j], w2[j + 1], w2[j + 2], w2[j + 3]);
+      for (int i = 0; i < 4; ++i) u[i] = uint32_t((live ? __float2int_rn((x[j + i] * sc_a) * sc_b) : 0) + 0x808080);
+      const uint32_t lo01 = __byte_perm(u[0], u[1], 0x5140);  // b0(u0) b0(u1) b1(u0) b1(u1)
+      const uint32_t lo23 = __byte_perm(u[2], u[3], 0x5140);
+      const uint32_t hi01 = __byte_perm(u[0], u[1], 0x7362);  // b2(u0) b2(u1) b3 b3
+      const uint32_t hi23 = __byte_perm(u[2], u[3], 0x7362);
+      w2[j / 4] = __byte_perm(lo01, lo23, 0x5410) ^ 0x80808080u;  // byte 0 of each u: low digit
+      w1[j / 4] = __byte_perm(lo01, lo23, 0x7632) ^ 0x80808080u;  // byte 1: middle digit
+      w0[j / 4] = __byte_perm(hi01, hi23, 0x5410) ^ 0x80808080u;  // byte 2: high digit
     }
-  } else {
+    int8_t* l0 = limbs + m * K_pad + k0;
+    int8_t* l1 = limbs + (M_pad + m) * K_pad + k0;
+    int8_t* l2 = limbs + (2 * M_pad + m) * K_pad + k0;
+    if constexpr (EPT % 16 == 0) {
 #pragma unroll
-    for (int j = 0; j < EPT / 4; ++j) {
-      reinterpret_cast<uint32_t*>(l0)[j] = w0[j];
-      reinterpret_cast<uint32_t*>(l1)[j] = w1[j];
-      reinterpret_cast<uint32_t*>(l2)[j] = w2[j];
+      for (int j = 0; j < EPT / 4; j += 4) {
+        reinterpret_cast<uint4*>(l0)[j / 4] = make_uint4(w0[j], w0[j + 1], w0[j + 2], w0[j + 3]);
+        reinterpret_cast<uint4*>(l1)[j / 4] = make_uint4(w1[j], w1[j + 1], w1[j + 2], w1[j + 3]);
+        reinterpret_cast<uint4*>(l2)[j / 4] = make_uint4(w2[j], w2[j + 1], w2[j + 2], w2[j + 3]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < EPT / 4; ++j) {
+        reinterpret_cast<uint32_t*>(l0)[j] = w0[j];
+        reinterpret_cast<uint32_t*>(l1)[j] = w1[j];
+        reinterpret_cast<uint32_t*>(l2)[j] = w2[j];
+      }
+    }
+  }
+  big = __reduce_add_sync(0xffffffffu, big);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&red_b[0], big);
+    __threadfence_block();
+    if (atomicAdd(&red_b[1], 1) == NW - 1) {  // last warp: every count is in
+      big = atomicAdd(&red_b[0], 0);
+      // amax / rms(nonzeros) > kWideRatio  <=>  nz * amax^2 > kWideRatio^2 * sum x^2; few entries near amax
+      const bool is_wide = live && (double(nz) * double(amax) * double(amax) > double(kWideRatio * kWideRatio) * s2 ||
+                                    big * kWideFrac < nz || s > kMaxScaleExp || s < -kMaxScaleExp);
+      const double sc = live ? ldexp(1.0, -s) : 0.0;
+      rscale[m] = is_wide ? -sc : sc;
+      TG_GT(1);
     }
   }
 }

@@ -1,0 +1,84 @@
+"""Seeded randomized sweep of the tensor-core path: random shapes (M, K, N), densities
+and variants, integer-valued X (the limbs and the int32 accumulation are exact, so Y
+must equal the reference-order gather path bit for bit), device-resident and
+host-streamed inputs.  Catches tile / cluster / split-K / decoder-group / chunking
+corner cases that the hand-picked shapes of test_gpu_paths.py may miss."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+CASES = int(__import__("os").environ.get("TG_FUZZ_CASES", "60"))
+
+
+@pytest.fixture(scope="module")
+def tg():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2510_06957_b200 as m
+
+    return m
+
+
+def _case(i):
+    rng = np.random.default_rng(1000 + i)
+    M = int(rng.choice([1, 3, 16, 17, 31, 48, 64, 65, 100, 129, 200, 257, 513]))
+    K = int(rng.choice([1, 5, 127, 128, 129, 300, 512, 1000, 2048, 4100]))
+    N = int(4 * rng.integers(1, 200))
+    dens = float(rng.choice([0.02, 0.1, 0.5, 0.9]))
+    u = rng.random((K, N))
+    W = np.where(u < dens / 2, 1, np.where(u < dens, -1, 0)).astype(np.int8)
+    X = rng.integers(-8, 9, size=(M, K)).astype(np.float32)
+    b = rng.integers(-8, 9, size=N).astype(np.float32)
+    variant = str(rng.choice(["base", "blocked", "interleaved_blocked", "vectorized_optimal", "horizontal"]))
+    alpha = 0.25 if variant in ("vectorized_optimal", "horizontal") and rng.random() < 0.7 else None
+    return M, K, N, W, X, b, variant, alpha
+
+
+@pytest.mark.parametrize("i", range(CASES))
+def test_fuzz_mma_equals_reference_order(tg, i):
+    M, K, N, W, X, b, variant, alpha = _case(i)
+    Wd = torch.from_numpy(W).cuda()
+    cfg = tg.GemmConfig(alpha=alpha, b=max(1, K // 2) if variant == "blocked" else None)
+    spec = tg.get_variant(variant)
+    fmt = spec.build(tg.TernaryDense(Wd), cfg)
+    outs = {}
+    for method in ("gather", "mma"):
+        c = tg.GemmConfig(alpha=alpha, method=method, b=cfg.b)
+        xd = spec.prepare(tg.DenseMatrix(torch.from_numpy(X).cuda()))
+        outs[method] = spec.run(xd, fmt, tg.BiasVector(b), c, False).values.copy()
+    assert np.array_equal(outs["mma"], outs["gather"]), (M, K, N, variant, alpha)
+    # the public call on host memory (streamed when large enough) gives the same bits
+    c = tg.GemmConfig(alpha=alpha, method="mma", b=cfg.b)
+    xh = spec.prepare(tg.DenseMatrix(torch.from_numpy(X).pin_memory()))
+    y = spec.run(xh, fmt, tg.BiasVector(b), c, False).values
+    assert np.array_equal(y, outs["gather"]), (M, K, N, variant, alpha, "host")
+
+
+@pytest.mark.parametrize("i", range(CASES))
+def test_fuzz_mma_real_x_within_tolerance(tg, i):
+    """Real-valued X (some rows with a wide dynamic range): the tensor-core path stays
+    within the 1e-5 normwise bar of the fp64 oracle (TOL as in test_gpu_parity.py)."""
+    TOL = 1e-5
+    M, K, N, W, _, b, variant, alpha = _case(i)
+    rng = np.random.default_rng(5000 + i)
+    X = rng.standard_normal((M, K)).astype(np.float32)
+    if M > 2 and K > 2:
+        X[M // 2, K // 3] *= 1e4  # a wide row: exact-order fix-up
+    b = b + rng.standard_normal(N).astype(np.float32)
+    Wd = torch.from_numpy(W).cuda()
+    c = tg.GemmConfig(alpha=alpha, method="mma", b=max(1, K // 2) if variant == "blocked" else None)
+    spec = tg.get_variant(variant)
+    fmt = spec.build(tg.TernaryDense(Wd), c)
+    y = spec.run(spec.prepare(tg.DenseMatrix(torch.from_numpy(X).cuda())), fmt, tg.BiasVector(b), c, False).values
+    ref = torch.from_numpy(X).cuda().double() @ Wd.double() + torch.from_numpy(b).cuda().double()
+    if alpha is not None:
+        ref = torch.where(ref > 0, ref, alpha * ref)
+    ref = ref.cpu().numpy()
+    den = np.abs(ref).max()
+    err = np.abs(y.astype(np.float64) - ref).max() / den if den > 0 else np.abs(y).max()
+    assert err <= TOL, (M, K, N, variant, alpha, err)
