@@ -62,6 +62,7 @@ METHODS = ("auto", "gather", "mma")
 # "auto" uses the tensor-core path when at least 1 in AUTO_MMA_MIN_DENSITY_INV
 # entries of W is nonzero (dense MACs per useful add <= 64).
 AUTO_MMA_MIN_DENSITY_INV = 64
+AUTO_MMA_MIN_TERMS = 64  # and at least this many nonzeros per output column on average
 
 
 class OpCount(NamedTuple):
@@ -265,6 +266,11 @@ def choose_method(method: str, K: int, N: int, nnz: int) -> str:
     if method != "auto":
         return method
     if K > (1 << 24):
+        return "gather"
+    # few terms per output: the reference-order gather is cheap there, and it keeps every
+    # output exact in the |terms|-scaled sense (the 22-bit row grid of the tensor-core
+    # path is relative to the row maximum, which a handful of small terms need not reach)
+    if nnz < AUTO_MMA_MIN_TERMS * N:
         return "gather"
     return "mma" if nnz * AUTO_MMA_MIN_DENSITY_INV >= K * N else "gather"
 

@@ -82,3 +82,41 @@ def test_fuzz_mma_real_x_within_tolerance(tg, i):
     den = np.abs(ref).max()
     err = np.abs(y.astype(np.float64) - ref).max() / den if den > 0 else np.abs(y).max()
     assert err <= TOL, (M, K, N, variant, alpha, err)
+
+
+@pytest.mark.parametrize("i", range(CASES))
+def test_fuzz_auto_adversarial_rows(tg, i):
+    """Rows built to stress a per-row fixed-point grid (bimodal magnitudes, a few large
+    outliers, log-uniform magnitudes over e^+-8, tiny or huge rows) with sparse and dense W.
+    Under method="auto" every output must meet both bars of SURVEY 8(c): normwise <= 1e-5
+    and |terms|-scaled elementwise <= 1e-5 (outputs with few terms take the exact gather)."""
+    TOL = 1e-5
+    rng = np.random.default_rng(9000 + i)
+    M = int(rng.choice([8, 33, 64, 130]))
+    K = int(rng.choice([64, 128, 256, 1024, 4096]))
+    N = int(4 * rng.integers(1, 64))
+    dens = float(rng.choice([0.02, 0.05, 0.2, 0.5]))
+    u = rng.random((K, N))
+    W = np.where(u < dens / 2, 1, np.where(u < dens, -1, 0)).astype(np.int8)
+    X = rng.standard_normal((M, K)).astype(np.float32)
+    pat = i % 4
+    if pat == 0:
+        X = np.where(rng.random((M, K)) < 0.5, X * 1e4, X).astype(np.float32)
+    elif pat == 1:
+        for m in range(M):
+            X[m, rng.choice(K, size=int(rng.integers(2, 4)), replace=False)] *= 3e3
+    elif pat == 2:
+        X = (X * np.exp(rng.uniform(-8, 8, size=(M, K)))).astype(np.float32)
+    else:
+        X *= np.float32(rng.choice([1e-30, 1e-12, 1e12, 1e30]))
+    b = rng.standard_normal(N).astype(np.float32) * np.float32(np.abs(X).mean())
+    Wd = torch.from_numpy(W).cuda()
+    fmt = tg.interleaved_blocked_from_dense(Wd, None, 2, True)
+    y = tg.gemm_vectorized_optimal(tg.pad_input(torch.from_numpy(X).cuda()), fmt, b, 0.25).values
+    Xd, Wdd, bd = torch.from_numpy(X).double(), torch.from_numpy(W).double(), torch.from_numpy(b).double()
+    ref = Xd @ Wdd + bd
+    terms = (Xd.abs() @ Wdd.abs() + bd.abs()).numpy()
+    ref = torch.where(ref > 0, ref, 0.25 * ref).numpy()
+    err = np.abs(y.astype(np.float64) - ref)
+    assert err.max() <= TOL * max(np.abs(ref).max(), 1e-300), (i, pat, M, K, N, dens)
+    assert (err <= TOL * terms).all(), (i, pat, M, K, N, dens, (err / np.maximum(terms, 1e-300)).max())
