@@ -46,12 +46,14 @@ def test_fuzz_mma_equals_reference_order(tg, i):
     cfg = tg.GemmConfig(alpha=alpha, b=max(1, K // 2) if variant == "blocked" else None)
     spec = tg.get_variant(variant)
     fmt = spec.build(tg.TernaryDense(Wd), cfg)
-    outs = {}
+    outs, counts = {}, {}
     for method in ("gather", "mma"):
         c = tg.GemmConfig(alpha=alpha, method=method, b=cfg.b)
         xd = spec.prepare(tg.DenseMatrix(torch.from_numpy(X).cuda()))
-        outs[method] = spec.run(xd, fmt, tg.BiasVector(b), c, False).values.copy()
+        y, ops = spec.run(xd, fmt, tg.BiasVector(b), c, True)
+        outs[method], counts[method] = y.values.copy(), ops
     assert np.array_equal(outs["mma"], outs["gather"]), (M, K, N, variant, alpha)
+    assert counts["mma"] == counts["gather"], (M, K, N, variant, alpha, counts)  # adds and PReLU mults
     # the public call on host memory (streamed when large enough) gives the same bits
     c = tg.GemmConfig(alpha=alpha, method="mma", b=cfg.b)
     xh = spec.prepare(tg.DenseMatrix(torch.from_numpy(X).pin_memory()))
@@ -120,3 +122,41 @@ def test_fuzz_auto_adversarial_rows(tg, i):
     err = np.abs(y.astype(np.float64) - ref)
     assert err.max() <= TOL * max(np.abs(ref).max(), 1e-300), (i, pat, M, K, N, dens)
     assert (err <= TOL * terms).all(), (i, pat, M, K, N, dens, (err / np.maximum(terms, 1e-300)).max())
+
+
+@pytest.mark.parametrize("i", range(CASES))
+def test_fuzz_device_builders_match_oracle(tg, i):
+    """Device builders against the C oracle (itself pinned to the reference) for random
+    shapes, block sizes, group sizes and sign balances: every index array bit for bit."""
+    from oracle import oracle as orc
+
+    rng = np.random.default_rng(7000 + i)
+    K = int(rng.integers(1, 700))
+    N = int(4 * rng.integers(1, 80)) if rng.random() < 0.7 else int(rng.integers(1, 300))
+    p_pos, p_neg = float(rng.random() * 0.6), float(rng.random() * 0.6)
+    u = rng.random((K, N))
+    W = np.where(u < p_pos, 1, np.where(u < min(1.0, p_pos + p_neg), -1, 0)).astype(np.int8)
+    Wd = tg.TernaryDense(torch.from_numpy(W).cuda())
+    B = int(rng.choice([1, 3, 16, 128, 4096])) if rng.random() < 0.8 else None
+    g = int(rng.integers(1, 5))
+
+    t, r = tg.tcsc_from_dense(Wd), orc.tcsc_from_dense(W)
+    for k in ("col_start_pos", "row_index_pos", "col_start_neg", "row_index_neg"):
+        assert np.array_equal(getattr(t, k), r[k]), ("tcsc", k)
+    bl, rb = tg.blocked_from_dense(Wd, B), orc.blocked_from_dense(W, B)
+    for k in ("col_start_pos", "row_index_pos", "col_start_neg", "row_index_neg"):
+        assert np.array_equal(getattr(bl, k), rb[k]), ("blocked", k)
+    sym_ok = N % 4 == 0
+    for sym in ((False, True) if sym_ok else (False,)):
+        ib, ri = tg.interleaved_blocked_from_dense(Wd, B, g, symmetric_cols=sym), \
+            orc.interleaved_blocked_from_dense(W, B, g, sym)
+        assert np.array_equal(ib.all_indices, ri["all_indices"]), ("ib", sym, K, N, B, g)
+        assert np.array_equal(ib.col_segment_ptr, ri["col_segment_ptr"]), ("ib ptr", sym)
+    if sym_ok:
+        sy, rs = tg.symmetric_from_dense(Wd, g), orc.symmetric_from_dense(W, g)
+        assert np.array_equal(sy.indices, rs["indices"]) and np.array_equal(sy.col_ptr, rs["col_ptr"])
+    cp, rc = tg.compressed_from_dense(Wd), orc.compressed_from_dense(W)
+    assert np.array_equal(cp.codes, rc["codes"])
+    # every format decodes back to W on the device
+    for f in (t, bl, cp):
+        assert np.array_equal(f.to_dense().values, W)
