@@ -160,3 +160,50 @@ def test_fuzz_device_builders_match_oracle(tg, i):
     # every format decodes back to W on the device
     for f in (t, bl, cp):
         assert np.array_equal(f.to_dense().values, W)
+
+
+@pytest.mark.parametrize("i", range(CASES))
+def test_fuzz_gather_bit_exact_with_reference_kernels(tg, i):
+    """The gather path against the C restatement of every reference kernel (pinned bit for
+    bit to the reference's own outputs) on real-valued X: identical fp32 bits, for random
+    shapes, block sizes, group sizes, unroll factors and row unrolls."""
+    from oracle import oracle as orc
+
+    rng = np.random.default_rng(11000 + i)
+    M = int(rng.integers(1, 70))
+    K = int(rng.integers(1, 600))
+    N = int(4 * rng.integers(1, 40))
+    u = rng.random((K, N))
+    d = float(rng.random())
+    W = np.where(u < d / 2, 1, np.where(u < d, -1, 0)).astype(np.int8)
+    X = (rng.standard_normal((M, K)) * np.exp(rng.uniform(-3, 3, size=(M, 1)))).astype(np.float32)
+    b = rng.standard_normal(N).astype(np.float32)
+    Wd = tg.TernaryDense(torch.from_numpy(W).cuda())
+    Xd = torch.from_numpy(X).cuda()
+    B = int(rng.choice([1, 7, 64, 4096]))
+    g = int(rng.integers(1, 4))
+    uf = int(rng.integers(1, 9))
+    mr = int(rng.choice([1, 2, 4]))
+    alpha = 0.25 if rng.random() < 0.5 else None
+    G = "gather"
+    t, r = tg.tcsc_from_dense(Wd), orc.tcsc_from_dense(W)
+    assert np.array_equal(tg.gemm_base(Xd, t, b, method=G).values, orc.gemm_base(X, r, b))
+    assert np.array_equal(tg.gemm_unrolled(Xd, t, b, tg.GemmConfig(uf=uf), method=G).values,
+                          orc.gemm_unrolled(X, r, b, uf=uf))
+    bl, rb = tg.blocked_from_dense(Wd, B), orc.blocked_from_dense(W, B)
+    assert np.array_equal(tg.gemm_blocked(Xd, bl, b, tg.GemmConfig(uf=uf, mr=mr), method=G).values,
+                          orc.gemm_blocked(X, rb, b, uf=uf, mr=mr))
+    ib, ri = tg.interleaved_blocked_from_dense(Wd, B, g), orc.interleaved_blocked_from_dense(W, B, g)
+    assert np.array_equal(tg.gemm_interleaved_blocked(Xd, ib, b, method=G).values,
+                          orc.gemm_interleaved_blocked(X, ri, b))
+    ibs, ris = tg.interleaved_blocked_from_dense(Wd, B, g, True), orc.interleaved_blocked_from_dense(W, B, g, True)
+    Xp = orc.pad_input(X)
+    assert np.array_equal(tg.gemm_vectorized_optimal(tg.pad_input(Xd), ibs, b, alpha, method=G).values,
+                          orc.gemm_vectorized_optimal(Xp, ris, b, alpha))
+    sy, rs = tg.symmetric_from_dense(Wd, g), orc.symmetric_from_dense(W, g)
+    assert np.array_equal(tg.gemm_vertical(tg.pad_input(Xd), sy, b, alpha, method=G).values,
+                          orc.gemm_vertical(Xp, rs, b, alpha))
+    assert np.array_equal(tg.gemm_horizontal(tg.pad_input(Xd), sy, b, alpha, method=G).values,
+                          orc.gemm_horizontal(Xp, rs, b, alpha))
+    cp, rc = tg.compressed_from_dense(Wd), orc.compressed_from_dense(W)
+    assert np.array_equal(tg.gemm_compressed(Xd, cp, b, method=G).values, orc.gemm_compressed(X, rc, b))
