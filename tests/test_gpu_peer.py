@@ -200,3 +200,43 @@ def test_scatter_rejects_bad_descriptors(tg):
             _runner(tg, W, X, b, None, out=torch.empty((M, N + 1), device="cuda"))
     finally:
         bufs.close()
+
+
+FUZZ = 30
+
+
+@pytest.mark.parametrize("i", range(FUZZ))
+def test_loopback_scatter_fuzz(tg, i):
+    """Random shapes, world sizes, shard offsets (aligned or not), PReLU and wide rows:
+    every loopback rank's assembled Y equals the unsharded GEMM bit for bit, two steps."""
+    from paper_2510_06957_b200.peer import PeerYBuffers, ScatterGemm
+
+    rng = np.random.default_rng(20000 + i)
+    world = int(rng.integers(1, 5))
+    M = int(rng.integers(1, 260))
+    K = int(rng.integers(1, 2500))
+    N = int(rng.integers(world, 1400))
+    alpha = 0.25 if rng.random() < 0.5 else None
+    wide = bool(rng.random() < 0.3) and M >= 3 and K >= 2
+    W, X, b = _setup(tg, M, K, N, seed=30000 + i, wide=wide)
+    ref = _full(tg, W, X, b, alpha)
+    views = PeerYBuffers.loopback(M, N, world)
+    gems = [ScatterGemm(lambda out, scatter, v=v: _runner(tg, W, X, b, alpha, cols=v.shard.slice(), out=out,
+                                                          scatter=scatter), v) for v in views]
+    try:
+        for step in range(2):
+            slot = gems[0].slot
+            for v in views:
+                v.y(slot).fill_(float("nan"))
+            torch.cuda.synchronize()
+            for gm in gems:
+                gm.runners[gm.slot].launch()
+            for gm in gems:
+                gm.bufs.wait()
+                gm.n += 1
+            torch.cuda.synchronize()
+            for v in views:
+                assert torch.equal(v.y(slot), ref), (i, step, v.rank, M, K, N, world)
+                assert not v.timed_out()
+    finally:
+        views[0].close()
