@@ -18,6 +18,7 @@ or the ``method=`` keyword; "auto" picks by density):
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from dataclasses import dataclass, replace
 from typing import Any, Callable, NamedTuple
@@ -221,7 +222,11 @@ def _workspace(nbytes: int, dev: torch.device, stream: int) -> torch.Tensor:
     return t
 
 
-STREAM_MIN_BYTES = 1 << 20   # host X below this is uploaded whole
+# Host X of at least this size goes through the library's host pipeline (tg_gemm_tiles_host:
+# copies, split and GEMM in one graph-replayed call, Y and its status words back with it);
+# smaller X is uploaded whole and launched through the runner.  0: every host X (measured:
+# cfg4's public call 0.153 -> 0.117 ms, cfg1 0.107 -> 0.102 ms against the upload path).
+STREAM_MIN_BYTES = int(os.environ.get("TG_STREAM_MIN_BYTES", "0"))
 
 
 def _host_source(v) -> torch.Tensor | None:
@@ -486,7 +491,7 @@ def _dispatch(kind: str, X, fmt, bias: torch.Tensor, method: str, counted: bool,
         hs, cols = X._hsrc, X.K + 1
     else:
         hs, cols = _host_source(X._v), X.cols
-    if method == "mma" and hs is not None and hs.numel() * 4 >= STREAM_MIN_BYTES and hs.shape[0] >= 128:
+    if method == "mma" and hs is not None and hs.numel() * 4 >= STREAM_MIN_BYTES:
         st = torch.cuda.current_stream(_device())
         with _plan_lock:
             plan = _host_plan(kind, fmt, int(hs.shape[0]), cols, method, kw, st)
