@@ -438,7 +438,10 @@ int enqueue_host(const HostKey& k, const HostPlan& P, SideStreams* ss, cudaStrea
     e = cudaMemset2DAsync(k.X_dev + k.K, size_t(k.ldx_dev) * 4, 0, size_t(k.ldx_dev - k.K) * 4, size_t(k.M), main);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaMemset2DAsync(padded slot)");
   }
-  if ((e = cudaEventRecord(ss->fork, main)) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
+  // One chunk: everything on the caller's stream (no fork / join edges to resolve).
+  const bool single = P.n == 1;
+  cudaStream_t sin = single ? main : ss->cin, sout = single ? main : ss->cout;
+  if (!single && (e = cudaEventRecord(ss->fork, main)) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
 #ifdef TG_TRACE
   if (!g_host_ev0) cudaEventCreate(&g_host_ev0);
   cudaEventRecord(g_host_ev0, main);
@@ -446,10 +449,10 @@ int enqueue_host(const HostKey& k, const HostPlan& P, SideStreams* ss, cudaStrea
   // Copies go through two in-order streams: issued from independent streams (or
   // as independent graph nodes) the copy engines may take the chunks in any
   // order or interleave them, and the first chunk's GEMM then starts last.
-  for (int i = 0; i < P.streams; ++i)
+  for (int i = 0; i < P.streams && !single; ++i)
     if ((e = cudaStreamWaitEvent(ss->s[i], ss->fork, 0)) != cudaSuccess) return set_cuda_error(e, "fork");
-  if ((e = cudaStreamWaitEvent(ss->cin, ss->fork, 0)) != cudaSuccess ||
-      (e = cudaStreamWaitEvent(ss->cout, ss->fork, 0)) != cudaSuccess)
+  if (!single && ((e = cudaStreamWaitEvent(ss->cin, ss->fork, 0)) != cudaSuccess ||
+                  (e = cudaStreamWaitEvent(ss->cout, ss->fork, 0)) != cudaSuccess))
     return set_cuda_error(e, "fork");
   const tg_format_ref* exact = k.has_exact ? &k.exact : nullptr;
   const int64_t M = k.M, K = k.K, N = k.N;
@@ -484,53 +487,55 @@ int enqueue_host(const HostKey& k, const HostPlan& P, SideStreams* ss, cudaStrea
     const int64_t r0 = c * P.rows, rows = std::min(P.rows, M - r0);
     float* xd = k.X_dev + r0 * k.ldx_dev;
     e = k.ldx_dev == K && k.ldx_host == K
-            ? cudaMemcpyAsync(xd, k.X_host + r0 * K, size_t(rows * K) * 4, cudaMemcpyHostToDevice, ss->cin)
+            ? cudaMemcpyAsync(xd, k.X_host + r0 * K, size_t(rows * K) * 4, cudaMemcpyHostToDevice, sin)
             : cudaMemcpy2DAsync(xd, size_t(k.ldx_dev) * 4, k.X_host + r0 * k.ldx_host, size_t(k.ldx_host) * 4,
-                                size_t(K) * 4, size_t(rows), cudaMemcpyHostToDevice, ss->cin);
+                                size_t(K) * 4, size_t(rows), cudaMemcpyHostToDevice, sin);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaMemcpy2DAsync(X chunk)");
-    if ((e = cudaEventRecord(ss->xin[c], ss->cin)) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
-    TG_HOST_EV(c, 0, ss->cin);
+    if (!single && (e = cudaEventRecord(ss->xin[c], sin)) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
+    TG_HOST_EV(c, 0, sin);
   }
   for (int64_t c = 0; c < P.n; ++c) {  // GEMMs side by side, each on 1/P.streams of the SMs
     const int i = int(c % P.streams);
-    cudaStream_t st = ss->s[i];
+    cudaStream_t st = single ? main : ss->s[i];
     const int64_t r0 = c * P.rows, rows = std::min(P.rows, M - r0);
     const float* xd = xh ? xh + r0 * k.ldx_host : k.X_dev + r0 * k.ldx_dev;
     const int64_t ldx = xh ? k.ldx_host : k.ldx_dev;
     float* yd = k.Y_dev + r0 * k.ldy_dev;
     void* wsi = static_cast<uint8_t*>(k.ws) + size_t(i) * P.ws_slice;
-    if (!xh && (e = cudaStreamWaitEvent(st, ss->xin[c], 0)) != cudaSuccess) return set_cuda_error(e, "wait X chunk");
+    if (!xh && !single && (e = cudaStreamWaitEvent(st, ss->xin[c], 0)) != cudaSuccess)
+      return set_cuda_error(e, "wait X chunk");
     TG_TRY(tg_gemm_tiles_prepare(xd, rows, K, ldx, wsi, P.ws_slice, k.flags, st));
     TG_HOST_EV(c, 3, st);
     TG_TRY(gemm_tiles_run(xd, rows, K, ldx, k.tiles, N, k.bias, yd, k.ldy_dev, k.use_alpha, k.alpha, exact,
                           nullptr, wsi, P.ws_slice, k.flags, st, P.streams, yh ? yh + r0 * k.ldy_host : nullptr,
                           k.ldy_host));
-    if ((e = cudaEventRecord(ss->ydone[c], st)) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
+    if (!single && (e = cudaEventRecord(ss->ydone[c], st)) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
     TG_HOST_EV(c, 1, st);
   }
   for (int64_t c = 0; c < P.n; ++c) {  // Y chunks out, in order
     const int64_t r0 = c * P.rows, rows = std::min(P.rows, M - r0);
     const float* yd = k.Y_dev + r0 * k.ldy_dev;
-    if ((e = cudaStreamWaitEvent(ss->cout, ss->ydone[c], 0)) != cudaSuccess) return set_cuda_error(e, "wait Y");
+    if (!single && (e = cudaStreamWaitEvent(ss->cout, ss->ydone[c], 0)) != cudaSuccess)
+      return set_cuda_error(e, "wait Y");
     if (yh) {  // already in host memory
-      TG_HOST_EV(c, 2, ss->cout);
+      TG_HOST_EV(c, 2, sout);
       continue;
     }
     e = k.ldy_dev == N && k.ldy_host == N
-            ? cudaMemcpyAsync(k.Y_host + r0 * N, yd, size_t(rows * N) * 4, cudaMemcpyDeviceToHost, ss->cout)
+            ? cudaMemcpyAsync(k.Y_host + r0 * N, yd, size_t(rows * N) * 4, cudaMemcpyDeviceToHost, sout)
             : cudaMemcpy2DAsync(k.Y_host + r0 * k.ldy_host, size_t(k.ldy_host) * 4, yd, size_t(k.ldy_dev) * 4,
-                                size_t(N) * 4, size_t(rows), cudaMemcpyDeviceToHost, ss->cout);
+                                size_t(N) * 4, size_t(rows), cudaMemcpyDeviceToHost, sout);
     if (e != cudaSuccess) return set_cuda_error(e, "cudaMemcpy2DAsync(Y chunk)");
-    TG_HOST_EV(c, 2, ss->cout);
+    TG_HOST_EV(c, 2, sout);
   }
-  for (int i = 0; i < P.streams; ++i) {
+  for (int i = 0; i < P.streams && !single; ++i) {
     if ((e = cudaEventRecord(ss->join[i], ss->s[i])) != cudaSuccess) return set_cuda_error(e, "cudaEventRecord");
     if ((e = cudaStreamWaitEvent(main, ss->join[i], 0)) != cudaSuccess) return set_cuda_error(e, "join");
   }
-  if ((e = cudaEventRecord(ss->join_in, ss->cin)) != cudaSuccess ||
+  if (!single && ((e = cudaEventRecord(ss->join_in, ss->cin)) != cudaSuccess ||
       (e = cudaEventRecord(ss->join_out, ss->cout)) != cudaSuccess ||
       (e = cudaStreamWaitEvent(main, ss->join_in, 0)) != cudaSuccess ||
-      (e = cudaStreamWaitEvent(main, ss->join_out, 0)) != cudaSuccess)
+      (e = cudaStreamWaitEvent(main, ss->join_out, 0)) != cudaSuccess))
     return set_cuda_error(e, "join");
   if (k.flags_host &&
       (e = cudaMemcpyAsync(k.flags_host, k.flags, sizeof(tg_device_flags), cudaMemcpyDeviceToHost, main)) !=
