@@ -234,7 +234,10 @@ class DenseMatrix:
                   done: torch.cuda.Event) -> "DenseMatrix":
         """A kernel output whose host copy (and status words) are already on their
         way through pinned memory; ``done`` marks their arrival."""
-        obj = cls(dev, _flags=host_flags)
+        obj = cls.__new__(cls)  # (dev is the library's own contiguous fp32 [M, N] output)
+        obj._flags = host_flags
+        obj._checked = False
+        obj._v = _Dual(None, dev)
         obj._arrival = (host, done)
         return obj
 
@@ -244,9 +247,9 @@ class DenseMatrix:
         _events.give(done)
         self._arrival = None
         f = self._flags
-        self._flags = f.clone()
+        self._flags = f.numpy().copy()  # (host words; the pinned buffer goes back to the pool)
         _pinned.give(f)
-        if _flags_bad(self._flags.numpy()):
+        if _flags_bad(self._flags):
             _pinned.give(host)
             raise ParameterError("dense matrix contains non-finite values")
         self._checked = True
@@ -263,7 +266,8 @@ class DenseMatrix:
             self._arrive()
         if not self._checked:
             if self._flags is not None:
-                bad = _flags_bad(self._flags.cpu().numpy())
+                f = self._flags
+                bad = _flags_bad(f if isinstance(f, np.ndarray) else f.cpu().numpy())
             else:
                 bad = not bool(torch.isfinite(self._v._d).all().item())
             if bad:

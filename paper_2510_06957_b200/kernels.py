@@ -431,7 +431,12 @@ class GemmRunner:
         dev = self.x.device
         if st is None:
             st = torch.cuda.current_stream(dev)
-        ws_bytes = nat.load().tg_gemm_host_workspace_bytes(self.M, self.K, self.N)  # (TG_HOST_CHUNKS may change)
+        chunks_env = os.environ.get("TG_HOST_CHUNKS")  # the chunk plan (and workspace) follows it
+        if self._ws is None or getattr(self, "_ws_env", None) != chunks_env:
+            ws_bytes = nat.load().tg_gemm_host_workspace_bytes(self.M, self.K, self.N)
+            self._ws_env = chunks_env
+        else:
+            ws_bytes = self._ws.numel()
         if self._ws is None or self._ws.numel() < ws_bytes:
             self._ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
         ws = self._ws
