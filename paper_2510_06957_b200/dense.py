@@ -24,9 +24,15 @@ from .errors import ParameterError
 EXACT_FLOAT32_BOUND = 2**24  # dense.py:17
 
 
+_cuda_seen = False
+
+
 def _device() -> torch.device:
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2510_06957_b200 needs a CUDA (sm_100a) device; there is no CPU path")
+    global _cuda_seen
+    if not _cuda_seen:  # is_available() costs microseconds per call; a device does not go away
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2510_06957_b200 needs a CUDA (sm_100a) device; there is no CPU path")
+        _cuda_seen = True
     return torch.device("cuda", torch.cuda.current_device())
 
 

@@ -497,7 +497,8 @@ def _dispatch(kind: str, X, fmt, bias: torch.Tensor, method: str, counted: bool,
     else:
         hs, cols = _host_source(X._v), X.cols
     if method == "mma" and hs is not None and hs.numel() * 4 >= STREAM_MIN_BYTES:
-        st = torch.cuda.current_stream(_device())
+        _device()
+        st = torch.cuda.current_stream()
         with _plan_lock:
             plan = _host_plan(kind, fmt, int(hs.shape[0]), cols, method, kw, st)
             y = plan.run_from_host(hs, bias, st)
