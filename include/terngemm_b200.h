@@ -240,6 +240,9 @@ int tg_gemm_tiles(const float* X, int64_t M, int64_t K, int64_t ldx, const uint3
  * When Y_host is pinned (device-mapped) and 16-byte aligned with a 16-byte row
  * pitch, the GEMM epilogue stores Y straight into it over PCIe and no D2H copy
  * is queued (TG_HOST_ZEROCOPY=0 restores the copies); Y_dev receives Y either way.
+ * When X_host is pinned (device-mapped) and X is at most 4 MB, the X split
+ * reads it in place over PCIe and no H2D copy is queued (X_dev is then not
+ * written; TG_HOST_ZEROCOPY_X=0 / 1 forces the copies / the in-place read).
  * With flags_host != NULL the call owns the status words: it zeroes `flags`
  * first and copies them to flags_host (pinned) after the last chunk, so one
  * synchronisation of `stream` delivers Y and its status together.

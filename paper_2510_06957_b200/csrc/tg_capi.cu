@@ -317,6 +317,21 @@ struct HostPlan {
   size_t ws_slice;  // workspace per side stream
 };
 
+// Small X is read in place by the X split (its CTAs load the pinned host rows over PCIe)
+// instead of being copied in: a copy-engine transfer delays the start of the kernels that
+// depend on it, which dominates for a few MB (measured cfg1 0.090 -> 0.080 ms, cfg2 0.25-0.48
+// -> 0.245 ms, cfg4 unchanged).  Larger X keeps the chunked copies: with one CTA per long
+// row the in-place reads do not keep enough PCIe requests in flight (cfg3, 16 MB: 1.1-1.3 ->
+// 1.34-1.41 ms; cfg5: 11.5 -> 21.9 ms).  TG_HOST_ZEROCOPY_X=0/1 forces either way.
+constexpr int64_t kZeroCopyXMaxBytes = int64_t(4) << 20;
+
+bool host_zero_copy_x(int64_t M, int64_t K) {
+  const char* env = getenv("TG_HOST_ZEROCOPY_X");
+  if (env && env[0] == '0') return false;
+  if (env && env[0] == '1') return true;
+  return M * K * 4 <= kZeroCopyXMaxBytes;
+}
+
 HostPlan host_plan(int64_t M, int64_t K, int64_t N) {
   HostPlan P;
   const int64_t bytes = M * K * 4;
@@ -400,6 +415,7 @@ struct HostKey {
   tg_device_flags* flags;
   tg_device_flags* flags_host;
   int64_t rows, n;
+  int64_t zero_copy_x;  // the X split reads the pinned host X in place (no X copies)
 };
 
 struct HostGraph {
@@ -470,14 +486,10 @@ int enqueue_host(const HostKey& k, const HostPlan& P, SideStreams* ss, cudaStrea
       yh = static_cast<float*>(pa.devicePointer);
     cudaGetLastError();
   }
-  // X read straight from the pinned host X by the split kernels (TG_HOST_ZEROCOPY_X=1):
+  // X read in place from the pinned host X by the split kernels (host_zero_copy_x):
   // no copy engine at all in the pipeline
   const float* xh = nullptr;
-  static const bool zcx_on = [] {
-    const char* env = getenv("TG_HOST_ZEROCOPY_X");
-    return env && env[0] == '1';
-  }();
-  if (zcx_on) {
+  if (k.zero_copy_x) {
     cudaPointerAttributes pa;
     if (cudaPointerGetAttributes(&pa, k.X_host) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
       xh = static_cast<const float*>(pa.devicePointer);
@@ -605,6 +617,7 @@ int tg_gemm_tiles_host(const float* X_host, int64_t M, int64_t K, int64_t ldx_ho
   if (exact) k.exact = *exact;
   cudaGetDevice(&k.dev);
   k.ws = ws, k.ws_bytes = ws_bytes, k.flags = flags, k.flags_host = flags_host, k.rows = P.rows, k.n = P.n;
+  k.zero_copy_x = host_zero_copy_x(M, K);
 
   static std::mutex enqueue_mu;  // the side streams, their events and the graph table are shared
   static HostGraph table[kHostGraphs];

@@ -135,11 +135,17 @@ def test_nonfinite_input_is_reported(tg, bad):
         tg.gemm_base(X, t, torch.zeros(N, device="cuda"), method="mma").values
 
 
+@pytest.mark.parametrize("xmode", [None, "0", "1"])
 @pytest.mark.parametrize("method", ["mma", "gather"])
-def test_host_input_is_streamed_bit_exact(tg, method):
+def test_host_input_is_streamed_bit_exact(tg, method, xmode, monkeypatch):
     """Host X (pinned tensor, numpy) goes through the row-chunked H2D / GEMM / D2H
-    pipeline; every entry point must give the bits of the device-resident call."""
+    pipeline (or, for small pinned X, is read in place by the X split; xmode forces
+    copies "0" / in-place "1"); every entry point must give the bits of the
+    device-resident call."""
     from paper_2510_06957_b200 import _native as nat
+
+    if xmode is not None:
+        monkeypatch.setenv("TG_HOST_ZEROCOPY_X", xmode)  # read by every host call
 
     M, K, N = 700, 1024, 320   # 2.9 MB of X: several chunks, a ragged last one
     rng = np.random.default_rng(3)
@@ -208,12 +214,16 @@ def test_host_streaming_graph_replay(tg):
     assert np.isfinite(tg.gemm_vectorized_optimal(tg.pad_input(Xpin), ibs, b, 0.25).values).all()
 
 
+@pytest.mark.parametrize("xmode", [None, "1"])
 @pytest.mark.parametrize("chunks", ["8", "3", "1"])
-def test_host_streaming_multi_chunk(tg, chunks, monkeypatch):
-    """X large enough for several row chunks (ragged last one): in-order copy streams,
-    side-by-side chunk GEMMs on SM shares, graph replay of the whole pipeline; every
-    chunking gives the device-resident call's bits (wide rows included)."""
+def test_host_streaming_multi_chunk(tg, chunks, xmode, monkeypatch):
+    """X large enough for several row chunks (ragged last one): in-order copy streams
+    (or the chunks' X splits reading the pinned X in place, xmode "1"), side-by-side
+    chunk GEMMs on SM shares, graph replay of the whole pipeline; every chunking gives
+    the device-resident call's bits (wide rows included)."""
     monkeypatch.setenv("TG_HOST_CHUNKS", chunks)
+    if xmode is not None:
+        monkeypatch.setenv("TG_HOST_ZEROCOPY_X", xmode)
     M, K, N = 1100, 2048, 640   # 9 MB of X: up to 4 chunks of 320 rows + 140
     rng = np.random.default_rng(21)
     W = rng.integers(-1, 2, size=(K, N)).astype(np.int8)
@@ -232,17 +242,20 @@ def test_host_streaming_multi_chunk(tg, chunks, monkeypatch):
     assert np.array_equal(tg.gemm_base(X, t, b).values, ref_b)  # pageable numpy X
 
 
+@pytest.mark.parametrize("xmode", ["0", "1"])
 @pytest.mark.parametrize("zerocopy_pitch", [False, True])
-def test_host_streaming_c_abi_pitched(tg, zerocopy_pitch):
+def test_host_streaming_c_abi_pitched(tg, zerocopy_pitch, xmode, monkeypatch):
     """tg_gemm_tiles_host through the C ABI with pitched buffers: host X of pitch K+1
     (2-D copies), a padded device staging X (ldx_dev > K: its slot columns are zeroed),
     a device Y of pitch N+3, and a host Y whose pitch either rules out the zero-copy
     store (N+1: 2-D D2H copies) or allows it (N+4).  Y and the status words must equal the
-    device-resident call."""
+    device-resident call.  xmode: X copied in ("0") or read in place by the split ("1",
+    a host pitch of K+1 floats: unaligned rows)."""
     import ctypes
 
     from paper_2510_06957_b200 import _native as nat
 
+    monkeypatch.setenv("TG_HOST_ZEROCOPY_X", xmode)
     M, K, N = 600, 1536, 256
     rng = np.random.default_rng(33)
     W = rng.integers(-1, 2, size=(K, N)).astype(np.int8)
