@@ -227,7 +227,7 @@ int tg_gemm_tiles(const float* X, int64_t M, int64_t K, int64_t ldx, const uint3
                   void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream);
 
 /* Host-resident X and Y: the reference's own calling convention (numpy in,
- * numpy out, dense.py:67-90).  X rows are streamed in chunks of about 2 MB;
+ * numpy out, dense.py:67-90).  X rows are streamed in chunks of about 1-2 MB;
  * each chunk's host->device copy (2-D, into the device staging X_dev of row
  * pitch ldx_dev, whose columns K..ldx_dev-1 are zeroed: the padded input's
  * slot, simd.py:72-75), X split + tile GEMM, and device->host copy of its Y

@@ -303,7 +303,7 @@ int tg_gemm_tiles(const float* X, int64_t M, int64_t K, int64_t ldx, const uint3
 // ------------------------------------------------------------------ GEMM from host memory
 namespace {
 
-// Row chunks of a host-resident X: about 2 MB of X each, at most 8, starting
+// Row chunks of a host-resident X: about 1-2 MB of X each, at most 8, starting
 // at multiples of 64 rows (a multiple of every blocked-order row unroll mr).
 // Small chunks let the two PCIe directions and the GEMMs overlap; what they
 // cost in host work is paid once, when the call is captured in a graph.  The
@@ -337,7 +337,11 @@ HostPlan host_plan(int64_t M, int64_t K, int64_t N) {
   const int64_t bytes = M * K * 4;
   int64_t cap = 8;
   if (const char* env = getenv("TG_HOST_CHUNKS")) cap = std::min(8, std::max(1, atoi(env)));  // (8 chunk events)
-  int64_t n = std::max<int64_t>(1, std::min<int64_t>({cap, bytes >> 21, M / 64}));
+  // ~1 MB chunks for X read in place (<= 4 MB; cfg2: 4 chunks 0.243 ms, 1 chunk 0.25-0.26 ms),
+  // ~2 MB for copied X (cfg3, 16 MB: 4 and 8 chunks within noise, 0.59-0.69 ms; cfg5: 8 chunks
+  // 11.7 ms, 4 chunks 12.5 ms)
+  const int64_t want = bytes <= kZeroCopyXMaxBytes ? bytes >> 20 : bytes >> 21;
+  int64_t n = std::max<int64_t>(1, std::min<int64_t>({cap, want, M / 64}));
   P.rows = round_up(ceil_div(M, n), 64);
   P.n = ceil_div(M, P.rows);
   P.streams = int(std::min<int64_t>(P.n, 4));
