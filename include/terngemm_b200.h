@@ -308,6 +308,15 @@ int tg_gemm_tiles_run_scatter(const float* X, int64_t M, int64_t K, int64_t ldx,
                               const tg_format_ref* exact, const tg_peer_scatter* scatter, void* ws,
                               size_t ws_bytes, tg_device_flags* flags, void* stream);
 
+/* ------------------------------------------------------------------ measurement probe
+ * Not on the GEMM path: the measured int8 tcgen05.mma rate of the current device, the
+ * denominator of bench.py's tensor roofline (tg_mma_kernel issues kind::i8 MMAs).  One
+ * persistent CTA per SM issues back-to-back M=128 x n x K=32 MMAs (A in smem or, with
+ * a_in_tmem, in TMEM as tg_mma_kernel does); `repeats` launches of `iters` x 16 MMAs per SM
+ * are timed with CUDA events.  n in {64, 128, 192, 256}.  Synchronous.                      */
+int tg_probe_i8_mma_rate(int n, int a_in_tmem, int iters, int repeats, double* ops_per_s /* host */,
+                         double* seconds /* host, may be NULL */);
+
 #ifdef __cplusplus
 }
 #endif

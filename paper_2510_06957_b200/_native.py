@@ -162,6 +162,7 @@ SIGNATURES: dict[str, tuple] = {
         _I,
         [_P, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _I, _F, _P, ctypes.POINTER(TgPeerScatter), _P, _SZ, _P, _P],
     ),
+    "tg_probe_i8_mma_rate": (_I, [_I, _I, _I, _I, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
 }
 
 _lock = threading.Lock()

@@ -117,6 +117,12 @@ def _to_host(d: torch.Tensor, extra: torch.Tensor | None = None):
     return _pinned.lease(h), f
 
 
+def _same_kind(other, cls) -> bool:
+    """Equality accepts this package's object or the reference's class of the same name
+    (dense.py:63-64 compares by class), so values round-trip between the two packages."""
+    return isinstance(other, cls) or (type(other).__name__ == cls.__name__ and hasattr(other, "values"))
+
+
 class _Dual:
     """Host/device pair with lazy, cached transfers."""
 
@@ -192,7 +198,7 @@ class TernaryDense:
         return int(torch.count_nonzero(self._v._d).item())
 
     def __eq__(self, other) -> bool:
-        return isinstance(other, TernaryDense) and np.array_equal(self.values, other.values)
+        return _same_kind(other, TernaryDense) and np.array_equal(self.values, np.asarray(other.values))
 
     def __repr__(self) -> str:
         return f"TernaryDense(K={self.K}, N={self.N})"
@@ -310,7 +316,7 @@ class DenseMatrix:
         return self._v.shape()[1]
 
     def __eq__(self, other) -> bool:
-        return isinstance(other, DenseMatrix) and np.array_equal(self.values, other.values)
+        return _same_kind(other, DenseMatrix) and np.array_equal(self.values, np.asarray(other.values))
 
     def __repr__(self) -> str:
         return f"DenseMatrix({self.rows}x{self.cols})"
@@ -349,11 +355,15 @@ class BiasVector:
         return self._v.shape()[0]
 
     def __eq__(self, other) -> bool:
-        return isinstance(other, BiasVector) and np.array_equal(self.values, other.values)
+        return _same_kind(other, BiasVector) and np.array_equal(self.values, np.asarray(other.values))
 
 
 def as_ternary(W) -> TernaryDense:
-    return W if isinstance(W, TernaryDense) else TernaryDense(W)
+    if isinstance(W, TernaryDense):
+        return W
+    if hasattr(W, "values") and not _is_tensor(W) and not isinstance(W, np.ndarray):
+        return TernaryDense(W.values)  # e.g. the reference's own TernaryDense
+    return TernaryDense(W)
 
 
 def as_dense(X) -> DenseMatrix:

@@ -8,11 +8,10 @@ unroll factors and are out of scope.
 
 from __future__ import annotations
 
-import statistics
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
-import torch
 
 from .errors import ParameterError, VerificationError
 
@@ -75,24 +74,22 @@ def verify(y: np.ndarray, ref: np.ndarray, exact: bool, label: str, tol: float =
     return a
 
 
-def time_device(fn, reps: int, warmup: int = 3, flush: torch.Tensor | None = None) -> list[float]:
-    """Per-call device time (ms) with CUDA events on the current stream; the L2
-    is flushed (``flush`` written) before every timed call, outside the events."""
-    for _ in range(warmup):
-        fn()
-    torch.cuda.synchronize()
-    out = []
-    for _ in range(reps):
-        if flush is not None:
-            flush.add_(1)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        fn()
-        e1.record()
-        e1.synchronize()
-        out.append(e0.elapsed_time(e1))
-    return out
+def measure_i8_mma_peak(n: int = 256, a_in_tmem: bool = False, seconds: float = 0.05,
+                        repeats: int = 4) -> dict:
+    """Measured int8 tcgen05.mma rate of the current device (``tg_probe_i8_mma_rate``,
+    csrc/tg_peak.cu): one persistent CTA per SM issuing back-to-back M=128 x n x K=32
+    kind::i8 MMAs.  ``seconds`` sizes each launch; ``repeats`` launches are timed
+    back to back with CUDA events (a ~0.2 s run gives the burst rate, a few seconds the
+    rate under the power cap).  Returns {"tops", "seconds", "n", "a"}."""
+    from . import _native
 
-
-def median(xs) -> float:
-    return float(statistics.median(xs))
+    lib = _native.load()
+    ops, sec = ctypes.c_double(), ctypes.c_double()
+    # calibrate the per-launch iteration count on a short run (~16 MMAs per iteration)
+    iters = 2000
+    _native.check(lib.tg_probe_i8_mma_rate(n, int(a_in_tmem), iters, 1, ctypes.byref(ops), ctypes.byref(sec)),
+                  "tg_probe_i8_mma_rate")
+    iters = max(1, int(iters * seconds / max(sec.value, 1e-6)))
+    _native.check(lib.tg_probe_i8_mma_rate(n, int(a_in_tmem), iters, repeats, ctypes.byref(ops),
+                                           ctypes.byref(sec)), "tg_probe_i8_mma_rate")
+    return {"tops": ops.value / 1e12, "seconds": sec.value, "n": n, "a": "tmem" if a_in_tmem else "smem"}
