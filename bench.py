@@ -629,8 +629,10 @@ def run_ours(args) -> None:
     def api_call():
         if sg is not None:
             xin.copy_(Xh_in, non_blocking=True)
-            y = sg.step()
-            return tg.DenseMatrix(y).values if rank == 0 else None
+            if rank != 0:
+                sg.step()
+                return None
+            return sg.result().values  # raises if the assembly's wait timed out
         if sym:
             y = tg.gemm_vectorized_optimal(tg.pad_input(Xh), fmt, tb, wl.alpha, method=method)
         elif kind == "interleaved_blocked":

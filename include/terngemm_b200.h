@@ -216,6 +216,10 @@ typedef struct {
  *     keep the limb result.
  * Bit-exact with the reference for integer-valued X; otherwise the only
  * rounding is X's 22-bit per-row grid and one final rounding (~1e-7 normwise).
+ * The tiles hold only real nonzeros: the symmetric formats' dummy indices
+ * (index K) are dropped, which equals the reference only while a padded
+ * input's slot X[:, K] is zero (the PaddedInput invariant, simd.py:40-70).
+ * The gather entry points read the slot as the reference does.
  * tg_gemm_tiles = prepare + run.                                               */
 int tg_gemm_tiles_prepare(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size_t ws_bytes,
                           tg_device_flags* flags, void* stream);

@@ -325,14 +325,22 @@ struct HostPlan {
 // 1.34-1.41 ms; cfg5: 11.5 -> 21.9 ms).  TG_HOST_ZEROCOPY_X=0/1 forces either way.
 constexpr int64_t kZeroCopyXMaxBytes = int64_t(4) << 20;
 
-bool host_zero_copy_x(int64_t M, int64_t K) {
+// In place only from pinned (device-mapped) host memory, and only where the split reads each
+// row once (xsplit_single_read): the decision is made before the chunk plan, which depends on it.
+bool host_zero_copy_x(const float* X_host, int64_t M, int64_t K) {
   const char* env = getenv("TG_HOST_ZEROCOPY_X");
-  if (env && env[0] == '0') return false;
-  if (env && env[0] == '1') return true;
-  return M * K * 4 <= kZeroCopyXMaxBytes;
+  bool want = M * K * 4 <= kZeroCopyXMaxBytes;
+  if (env && env[0] == '0') want = false;
+  if (env && env[0] == '1') want = true;
+  if (!want || !xsplit_single_read(K)) return false;
+  cudaPointerAttributes pa;
+  const bool mapped = cudaPointerGetAttributes(&pa, X_host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+                      pa.devicePointer != nullptr;
+  cudaGetLastError();
+  return mapped;
 }
 
-HostPlan host_plan(int64_t M, int64_t K, int64_t N) {
+HostPlan host_plan(int64_t M, int64_t K, int64_t N, bool x_in_place) {
   HostPlan P;
   const int64_t bytes = M * K * 4;
   int64_t cap = 8;
@@ -340,7 +348,7 @@ HostPlan host_plan(int64_t M, int64_t K, int64_t N) {
   // ~1 MB chunks for X read in place (<= 4 MB; cfg2: 4 chunks 0.243 ms, 1 chunk 0.25-0.26 ms),
   // ~2 MB for copied X (cfg3, 16 MB: 4 and 8 chunks within noise, 0.59-0.69 ms; cfg5: 8 chunks
   // 11.7 ms, 4 chunks 12.5 ms)
-  const int64_t want = bytes <= kZeroCopyXMaxBytes ? bytes >> 20 : bytes >> 21;
+  const int64_t want = x_in_place ? bytes >> 20 : bytes >> 21;
   int64_t n = std::max<int64_t>(1, std::min<int64_t>({cap, want, M / 64}));
   P.rows = round_up(ceil_div(M, n), 64);
   P.n = ceil_div(M, P.rows);
@@ -593,8 +601,9 @@ extern "C" {
 
 size_t tg_gemm_host_workspace_bytes(int64_t M, int64_t K, int64_t N) {
   if (M < 1 || K < 1 || N < 1) return 0;
-  const HostPlan P = host_plan(M, K, N);
-  return size_t(P.streams) * P.ws_slice;
+  // either plan may run (in place or copied X is decided per call): size for the larger
+  const HostPlan P0 = host_plan(M, K, N, false), P1 = host_plan(M, K, N, true);
+  return std::max(size_t(P0.streams) * P0.ws_slice, size_t(P1.streams) * P1.ws_slice);
 }
 
 int tg_gemm_tiles_host(const float* X_host, int64_t M, int64_t K, int64_t ldx_host, float* X_dev, int64_t ldx_dev,
@@ -609,7 +618,8 @@ int tg_gemm_tiles_host(const float* X_host, int64_t M, int64_t K, int64_t ldx_ho
              "leading dimensions too small");
   TG_REQUIRE(ws_bytes >= tg_gemm_host_workspace_bytes(M, K, N), TG_ERR_PARAM, "workspace too small");
   TG_TRY(require_device());
-  const HostPlan P = host_plan(M, K, N);
+  const bool x_in_place = host_zero_copy_x(X_host, M, K);
+  const HostPlan P = host_plan(M, K, N, x_in_place);
   SideStreams* ss = nullptr;
   TG_TRY(side_streams(&ss));
   HostKey k;
@@ -621,7 +631,7 @@ int tg_gemm_tiles_host(const float* X_host, int64_t M, int64_t K, int64_t ldx_ho
   if (exact) k.exact = *exact;
   cudaGetDevice(&k.dev);
   k.ws = ws, k.ws_bytes = ws_bytes, k.flags = flags, k.flags_host = flags_host, k.rows = P.rows, k.n = P.n;
-  k.zero_copy_x = host_zero_copy_x(M, K);
+  k.zero_copy_x = x_in_place;
 
   static std::mutex enqueue_mu;  // the side streams, their events and the graph table are shared
   static HostGraph table[kHostGraphs];

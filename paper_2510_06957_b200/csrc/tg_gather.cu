@@ -34,8 +34,9 @@ size_t gather_ws_bytes(int64_t M, int64_t K) {
   return size_t(K + 1) * size_t(round_up(M, G_ROWS)) * sizeof(float) + 256;
 }
 
-// X (M x ldx) -> Xt ((K+1) x M_pad), zero padded.
-__global__ void tg_transpose_kernel(const float* __restrict__ X, int64_t M, int64_t K, int64_t ldx,
+// X (M x ldx) -> Xt ((K+1) x M_pad), zero padded; columns k < Kx are read from X (Kx = K + 1
+// for a padded input: the dummy index K reads X[:, K] as the reference kernels do).
+__global__ void tg_transpose_kernel(const float* __restrict__ X, int64_t M, int64_t K, int64_t Kx, int64_t ldx,
                                     float* __restrict__ Xt, int64_t M_pad, tg_device_flags* flags) {
   __shared__ float tile[32][33];
   const int64_t k0 = int64_t(blockIdx.x) * 32, m0 = int64_t(blockIdx.y) * 32;
@@ -43,7 +44,7 @@ __global__ void tg_transpose_kernel(const float* __restrict__ X, int64_t M, int6
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const int64_t m = m0 + r, k = k0 + threadIdx.x;
     float v = 0.f;
-    if (m < M && k < K) {
+    if (m < M && k < Kx) {
       v = X[m * ldx + k];
       bad |= !isfinite(v);
     }
@@ -103,10 +104,10 @@ __global__ void __launch_bounds__(G_WARPS * 32)
   }
 }
 
-int run_transpose(const float* X, int64_t M, int64_t K, int64_t ldx, float* Xt, int64_t M_pad,
+int run_transpose(const float* X, int64_t M, int64_t K, int64_t Kx, int64_t ldx, float* Xt, int64_t M_pad,
                   tg_device_flags* flags, cudaStream_t st) {
   dim3 grid(unsigned(ceil_div(K + 1, 32)), unsigned(ceil_div(M_pad, 32)));
-  tg_transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(X, M, K, ldx, Xt, M_pad, flags);
+  tg_transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(X, M, K, Kx, ldx, Xt, M_pad, flags);
   return check_launch("tg_transpose_kernel");
 }
 
@@ -115,7 +116,9 @@ int run_gather_args(int variant, const float* X, int64_t M, int64_t K, int64_t l
                     tg_device_flags* flags, cudaStream_t st) {
   const int64_t M_pad = round_up(M, G_ROWS);
   float* Xt = static_cast<float*>(ws);
-  int rc = run_transpose(X, M, K, ldx, Xt, M_pad, flags, st);
+  // the PaddedInput variants (simd.py:40-75) read their dummy slot X[:, K] like the reference
+  const bool padded = variant == VAR_OPTIMAL || variant == VAR_VERTICAL || variant == VAR_HORIZONTAL;
+  int rc = run_transpose(X, M, K, (padded && ldx > K) ? K + 1 : K, ldx, Xt, M_pad, flags, st);
   if (rc != TG_OK) return rc;
   dim3 grid(unsigned(ceil_div(ga.N, G_WARPS)), unsigned(M_pad / G_ROWS));
 #define TG_GATHER_LAUNCH(V) \

@@ -20,6 +20,7 @@ inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
 struct GatherArgs;  // tg_walk.cuh
 int mma_pick_mt(int64_t M);
 size_t xsplit_bytes(int64_t M, int64_t K);
+bool xsplit_single_read(int64_t K);
 size_t mma_ws_bytes(int64_t M, int64_t K, int64_t N, int share = 1);
 int run_xsplit(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size_t ws_bytes, tg_device_flags* flags,
                cudaStream_t st);

@@ -32,6 +32,8 @@
 //                   order (tg_walk.cuh).
 #include <cuda.h>
 #include <cuda_runtime.h>
+
+#include <atomic>
 #include <cudaTypedefs.h>
 #include <cstdint>
 #include <cstdlib>
@@ -1354,12 +1356,27 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
+// Per-device caches: kernel attributes (cudaFuncSetAttribute) and occupancy apply per device
+// context, so every cache below is keyed by the current device (up to 64 devices).
+static int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev & 63;
+}
+
+// true once per (flag set, device): the caller then applies its per-device setup
+static bool first_on_device(std::atomic<uint64_t>& done) {
+  const uint64_t bit = uint64_t(1) << current_device();
+  return (done.fetch_or(bit) & bit) == 0;
+}
+
 static int num_sms() {
-  static int n = 0;
+  static std::atomic<int> cache[64];
+  const int d = current_device();
+  int n = cache[d].load(std::memory_order_relaxed);
   if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || n <= 0) n = 148;
+    cache[d].store(n, std::memory_order_relaxed);
   }
   return n;
 }
@@ -1415,7 +1432,9 @@ static int pick_cluster(int64_t mt, int64_t NB) {
 
 template <int MT, int CS>
 static int max_clusters() {
-  static int n = 0;
+  static std::atomic<int> cache[64];
+  const int d = current_device();
+  int n = cache[d].load(std::memory_order_relaxed);
   if (n == 0) {
     using C = MmaCfg<MT>;
     cudaFuncSetAttribute(tg_mma_kernel<MT, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -1437,6 +1456,7 @@ static int max_clusters() {
       c = num_sms() / CS;
     }
     n = c;
+    cache[d].store(n, std::memory_order_relaxed);
   }
   return n;
 }
@@ -1493,6 +1513,10 @@ static SplitLayout split_layout(int64_t M, int64_t K, int64_t N, int share = 1) 
 }
 
 size_t xsplit_bytes(int64_t M, int64_t K) { return split_layout(M, K, 0).total_prepare; }
+// true when the X split reads each row once (register- or smem-resident kernels); the
+// multi-pass fall-back for longer rows reads a row twice, which over PCIe (X read in place
+// from host memory) would double the transfer
+bool xsplit_single_read(int64_t K) { return split_layout(1, K, 0).K_pad <= 1024 * 32 || K <= XS_SMEM_MAX_K; }
 size_t mma_ws_bytes(int64_t M, int64_t K, int64_t N, int share) { return split_layout(M, K, N, share).total; }
 
 int run_xsplit(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size_t ws_bytes, tg_device_flags* flags,
@@ -1523,15 +1547,17 @@ int run_xsplit(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size
 #undef TG_XS_REG
   if (K <= XS_SMEM_MAX_K) {
     const size_t smem = size_t(round_up(K, 4)) * sizeof(float);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr_done{0};
+    if (first_on_device(attr_done)) {
       e = cudaFuncSetAttribute(tg_xsplit_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                int(XS_SMEM_MAX_K * sizeof(float)));
       if (e == cudaSuccess)
         e = cudaFuncSetAttribute(tg_xsplit_kernel<true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(XS_SMEM_MAX_K * sizeof(float)));
-      if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(tg_xsplit_kernel)");
-      attr = true;
+      if (e != cudaSuccess) {
+        attr_done.fetch_and(~(uint64_t(1) << current_device()));
+        return set_cuda_error(e, "cudaFuncSetAttribute(tg_xsplit_kernel)");
+      }
     }
     // few rows: more threads per row so the whole GPU has loads in flight
     if (L.M_pad <= 4 * num_sms())
@@ -1551,12 +1577,14 @@ template <int MT, int CS>
 static int launch_mma(const CUtensorMap& map, const CUtensorMap& ymap, const MmaParams& p, int grid,
                       cudaStream_t st) {
   using C = MmaCfg<MT>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_done{0};
+  if (first_on_device(attr_done)) {
     cudaError_t e =
         cudaFuncSetAttribute(tg_mma_kernel<MT, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(tg_mma_kernel)");
-    attr_set = true;
+    if (e != cudaSuccess) {
+      attr_done.fetch_and(~(uint64_t(1) << current_device()));
+      return set_cuda_error(e, "cudaFuncSetAttribute(tg_mma_kernel)");
+    }
   }
   MmaParams pp = p;
   if (C::Y_BYTES == 0) pp.tma_y = 0;  // no smem Y tile at this tile size

@@ -13,6 +13,7 @@ path never synchronises.
 from __future__ import annotations
 
 import threading
+from collections import deque
 from fractions import Fraction
 import weakref
 
@@ -94,6 +95,40 @@ class _EventPool:
 
 
 _events = _EventPool()
+
+
+class _Deferred:
+    """Pinned buffers of streamed results that were dropped before they arrived.
+
+    The library reads the host X and writes the pinned Y and status words through raw
+    pointers, so torch's caching host allocator records no stream use for them: freed on
+    the spot, they could be handed to the next ``pin_memory()`` while the copies (or the
+    epilogue's direct stores) are still in flight.  A result's finalizer parks them here
+    with the event that marks the end of those transfers; every new streamed call drains
+    the entries whose event has completed, returning Y and the status words to the pool."""
+
+    def __init__(self):
+        self._q: deque = deque()
+        self._lock = threading.Lock()
+
+    def park(self, box: list) -> None:
+        if box:  # empty once the result arrived normally
+            with self._lock:
+                self._q.append(tuple(box))
+            box.clear()
+
+    def drain(self) -> None:
+        done = []
+        with self._lock:
+            while self._q and self._q[0][1].query():
+                done.append(self._q.popleft())
+        for host, ev, flags, _keep in done:
+            _pinned.give(host)
+            _pinned.give(flags)
+            _events.give(ev)
+
+
+_deferred = _Deferred()
 
 
 def _to_host(d: torch.Tensor, extra: torch.Tensor | None = None):
@@ -204,10 +239,16 @@ class TernaryDense:
         return f"TernaryDense(K={self.K}, N={self.N})"
 
 
+PEER_TIMEOUT_BIT = 8  # bad_input bit 3: a fused shard assembly gave up waiting for a rank (peer.py)
+
+
 def _flags_bad(f) -> bool:
     """Kernel status words (tg_device_flags as int32): a non-finite output, or a
     non-finite X entry seen by the tensor-core split (bad_input bit 2; the
-    reference rejects such an X when it is constructed, dense.py:77)."""
+    reference rejects such an X when it is constructed, dense.py:77).  A peer
+    timeout (bit 3) is raised as its own error first."""
+    if int(f[0]) & PEER_TIMEOUT_BIT:
+        raise RuntimeError("fused shard assembly timed out: a rank never arrived, Y is incomplete")
     return int(f[1]) != 0 or (int(f[0]) & 4) != 0
 
 
@@ -243,19 +284,24 @@ class DenseMatrix:
 
     @classmethod
     def _streamed(cls, dev: torch.Tensor, host: torch.Tensor, host_flags: torch.Tensor,
-                  done: torch.cuda.Event) -> "DenseMatrix":
+                  done: torch.cuda.Event, keep: tuple = ()) -> "DenseMatrix":
         """A kernel output whose host copy (and status words) are already on their
-        way through pinned memory; ``done`` marks their arrival."""
+        way through pinned memory; ``done`` marks their arrival.  ``keep`` holds host
+        inputs the call reads in place (a pinned X) until then."""
         obj = cls.__new__(cls)  # (dev is the library's own contiguous fp32 [M, N] output)
         obj._flags = host_flags
         obj._checked = False
         obj._v = _Dual(None, dev)
-        obj._arrival = (host, done)
+        box = [host, done, host_flags, keep]
+        obj._arrival = box
+        weakref.finalize(obj, _deferred.park, box)  # dropped before arrival: park the buffers
         return obj
 
     def _arrive(self) -> None:
-        host, done = self._arrival
+        box = self._arrival
+        host, done = box[0], box[1]
         done.synchronize()
+        box.clear()  # arrived: nothing for the finalizer to park
         _events.give(done)
         self._arrival = None
         f = self._flags

@@ -33,6 +33,7 @@ from .dense import (
     TernaryDense,
     _device,
     _Dual,
+    _deferred,
     _events,
     _pinned,
     as_bias,
@@ -459,6 +460,7 @@ class GemmRunner:
             self._ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
         ws = self._ws
         b = self.bias if bias is None else bias
+        _deferred.drain()
         y = torch.empty((self.M, self.N), dtype=torch.float32, device=dev)
         y_host = _pinned.take((self.M, self.N), torch.float32)
         f_host = _pinned.take((6,), torch.int32)
@@ -468,7 +470,7 @@ class GemmRunner:
                  _p(ws), ws.numel(), _p(self.flags), ctypes.c_void_p(f_host.data_ptr()), st.cuda_stream)
         done = _events.take()
         done.record(st)
-        return DenseMatrix._streamed(y, y_host, f_host, done)
+        return DenseMatrix._streamed(y, y_host, f_host, done, keep=(hx,))
 
     def pin_workspace(self) -> None:
         """Give this runner a private workspace (needed for graph capture / concurrent replays)."""

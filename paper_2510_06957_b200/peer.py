@@ -40,6 +40,7 @@ import torch
 import torch.distributed as dist
 
 from . import _native as nat
+from .dense import PEER_TIMEOUT_BIT, DenseMatrix
 from .errors import ParameterError
 from .partition import Shard, column_shards
 
@@ -227,3 +228,14 @@ class ScatterGemm:
         self.bufs.wait(stream)
         self.n += 1
         return self.bufs.y(s)
+
+    def result(self) -> DenseMatrix:
+        """One step on the current stream, returned as a DenseMatrix whose status words carry
+        the runner's (non-finite output) and the wait's timeout word: reading ``.values`` or
+        ``check()`` raises if the wait gave up, instead of handing out a partly assembled Y."""
+        s = self.slot
+        y = self.step()
+        flags = self.runners[s].flags.clone()
+        timeout = self.bufs.header[nat.TG_PEER_TIMEOUT_WORD]
+        flags[0] = flags[0] | (timeout != 0).to(torch.int32) * PEER_TIMEOUT_BIT
+        return DenseMatrix(y, _flags=flags)

@@ -224,11 +224,14 @@ def test_host_streaming_multi_chunk(tg, chunks, xmode, monkeypatch):
     monkeypatch.setenv("TG_HOST_CHUNKS", chunks)
     if xmode is not None:
         monkeypatch.setenv("TG_HOST_ZEROCOPY_X", xmode)
-    M, K, N = 2100, 2048, 640   # 17 MB of X: up to 7 chunks of 320 rows (the last 180)
+    M, K, N = 2100, 2048, 640   # 17 MB of X: 8 chunks -> 7 of 320 rows (the last 180); 3 -> 704 rows
     rng = np.random.default_rng(21)
     W = rng.integers(-1, 2, size=(K, N)).astype(np.int8)
     X = rng.standard_normal((M, K)).astype(np.float32)
-    X[1300, 9] = 3e4  # a wide row inside the third chunk
+    # wide rows on both sides of the chunk boundaries of either plan (320- and 704-row chunks),
+    # inside a chunk, and the first and last rows
+    for r in (0, 319, 320, 703, 704, 1300, 1407, 1408, 2099):
+        X[r, 9] = 3e4
     b = rng.standard_normal(N).astype(np.float32)
     Wd = torch.from_numpy(W).cuda()
     ibs = tg.interleaved_blocked_from_dense(Wd, None, 2, True)

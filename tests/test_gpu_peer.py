@@ -169,9 +169,11 @@ def test_wait_gives_up_when_a_rank_never_arrives(tg):
     try:
         gm = ScatterGemm(lambda out, scatter: _runner(tg, W, X, b, None, cols=views[0].shard.slice(), out=out,
                                                       scatter=scatter), views[0])
-        gm.step()
+        res = gm.result()
         torch.cuda.synchronize()
         assert views[0].timed_out()
+        with pytest.raises(RuntimeError, match="timed out"):
+            res.values  # the result path reports the incomplete assembly
         hdr = views[1].header.cpu().numpy().view(np.uint32)
         assert hdr[0] == 1  # rank 0 still delivered its arrival to rank 1
     finally:
