@@ -710,7 +710,7 @@ int tg_gemm_blocked(const float* X, int64_t M, int64_t K, int64_t ldx, int64_t B
   TG_REQUIRE(csp && csn, TG_ERR_PARAM, "null offset table");
   const int64_t m_full = M / mr * mr;
   return run_gather(GATHER_BLOCKED, X, M, K, ldx, csp, rip, csn, rin, ceil_div(K, B), 1, uf, m_full, N, bias, Y,
-                    ldy, use_alpha, alpha, ws, flags, as_stream(stream));
+                    ldy, use_alpha, alpha, ws, flags, as_stream(stream), B);
 }
 
 int tg_gemm_interleaved_blocked(const float* X, int64_t M, int64_t K, int64_t ldx, int64_t B, int g,
@@ -724,7 +724,7 @@ int tg_gemm_interleaved_blocked(const float* X, int64_t M, int64_t K, int64_t ld
              "unknown order");
   return run_gather(order == TG_ORDER_INTERLEAVED_BLOCKED ? GATHER_IB : GATHER_OPTIMAL, X, M, K, ldx, ptr, ai,
                     nullptr, nullptr, ceil_div(K, B), g, 1, 0, N, bias, Y, ldy, use_alpha, alpha, ws, flags,
-                    as_stream(stream));
+                    as_stream(stream), B);
 }
 
 }  // extern "C"

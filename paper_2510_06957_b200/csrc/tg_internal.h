@@ -42,7 +42,7 @@ size_t gather_ws_bytes(int64_t M, int64_t K);
 int run_gather(int variant, const float* X, int64_t M, int64_t K, int64_t ldx, const int32_t* p0, const int32_t* i0,
                const int32_t* p1, const int32_t* i1, int64_t nblocks, int g, int uf, int64_t m_full, int64_t N,
                const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, void* ws,
-               tg_device_flags* flags, cudaStream_t st);
+               tg_device_flags* flags, cudaStream_t st, int64_t B = 0);
 
 
 }  // namespace tg

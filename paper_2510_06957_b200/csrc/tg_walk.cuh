@@ -153,6 +153,7 @@ struct GatherArgs {
   int g, uf;
   const uint8_t* codes;  // compressed: N x G packed base-3 codes
   int64_t G;
+  int64_t B = 0;  // block size in k (blocked / interleaved formats); 0 = one block over all of K
 };
 
 // Y[m, n] before the activation, in the reference's operation order for VAR.
