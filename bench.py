@@ -87,9 +87,31 @@ def peaks() -> dict:
     }
 
 
-def config_dict(cfg: str, nnz: int) -> dict:
+def parse_outliers(spec: str | None):
+    """--x-outliers "C@S": C activation channels at S x (LLM-style heavy tails); None: the BASELINE X."""
+    if not spec:
+        return None
+    c, s = spec.split("@")
+    return int(c), float(s)
+
+
+def bench_inputs(cfg: str, outliers: str | None = None, integer: bool = False):
+    """The config's seeded inputs; with --x-outliers the same seeded channels of X are scaled."""
+    W, X, b = make_inputs(cfg, integer=integer)
+    o = parse_outliers(outliers)
+    if o is not None and not integer:
+        ch = np.random.default_rng(20251006).choice(X.shape[1], o[0], replace=False)
+        X[:, ch] *= np.float32(o[1])
+    return W, X, b
+
+
+def config_dict(cfg: str, nnz: int, outliers: str | None = None) -> dict:
     """The workload description, identical in both arms (the driver compares them)."""
     wl = WORKLOADS[cfg]
+    if outliers:
+        d = config_dict(cfg, nnz)
+        d["x_outliers"] = f"{outliers}: channels x scale applied to the seeded X (not a BASELINE config)"
+        return d
     return {"workload": cfg, "M": wl.M, "K": wl.K, "N": wl.N, "p_nonzero": wl.p_pos + wl.p_neg, "nnz": nnz,
             "x_dist": wl.x_dist, "bias": wl.bias, "alpha": wl.alpha, "variant": wl.variant, "seed": wl.seed,
             "l2": "GPU arm: 256 MB L2 flush before every timed step, outside the events "
@@ -319,7 +341,7 @@ def run_reference(args) -> None:
         return
     cfg = args.config
     cores = len(os.sched_getaffinity(0))
-    cpu = CpuPath(cfg, cores)
+    cpu = CpuPath(cfg, cores, **(dict(zip("WXb", bench_inputs(cfg, args.x_outliers))) if args.x_outliers else {}))
     meas = cpu.measure(args.steps, args.warmup)
     value = meas["value"]
     line = {
@@ -327,7 +349,7 @@ def run_reference(args) -> None:
         "n_gpus": max(world, args.gpus), "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(meas["seconds_per_step"] * 1e3, 4), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (BASELINE.json recipe, seeded; no dataset)",
-        "config": config_dict(cfg, cpu.nnz),
+        "config": config_dict(cfg, cpu.nnz, args.x_outliers),
         "cpu_baseline": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in meas.items()},
         "e2e": {"value": round(value, 4), "unit": "GOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -397,7 +419,7 @@ def run_ours(args) -> None:
 
     cfg = args.config
     wl = WORKLOADS[cfg]
-    W, X, b = make_inputs(cfg)
+    W, X, b = bench_inputs(cfg, args.x_outliers)
     M, K, N = wl.M, wl.K, wl.N
     sym = wl.variant == "vectorized_optimal"
     part = ShardedGemm(M, N, "columns", symmetric=sym)
@@ -456,6 +478,9 @@ def run_ours(args) -> None:
           and (method != "gather" or "vs_cpu_reference" not in parity or parity["vs_cpu_reference"]["bit_exact"]))
     if max_over_ranks(0.0 if ok else 1.0, world, dev) != 0.0:
         raise SystemExit(f"refusing to time a wrong kernel: {json.dumps(parity)}")
+    # how the X split classified the rows (tensor-core path): rows left to the exact-order walk,
+    # rows that shed outlier entries into the epilogue's list
+    row_stats = runner.row_stats() if method == "mma" else None
 
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
     stream = torch.cuda.current_stream()
@@ -752,13 +777,13 @@ def run_ours(args) -> None:
     launches_per_step = 2  # mma: X split + tile MMA; gather: transpose + gather
     if sg is not None:
         launches_per_step = 3  # + the arrival wait
-    conf = config_dict(cfg, nnz_total)
+    conf = config_dict(cfg, nnz_total, args.x_outliers)
     line = {
         "metric": "effective_gops", "value": round(value, 3), "unit": "GOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(t_step_max, 5), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (BASELINE.json recipe, seeded; no dataset)",
         "config": conf,
-        "run": {"method": method,
+        "run": {"method": method, "x_rows": row_stats,
                 "parallelism": f"N-sharded x{world}" + (
                     "" if world == 1 else " + fused peer-store epilogue over NVLink" if assembly == "peer"
                     else " + NCCL all-gather"),
@@ -797,6 +822,8 @@ def main() -> None:
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(WORKLOADS))
     ap.add_argument("--method", default="auto", choices=("auto", "mma", "gather"))
+    ap.add_argument("--x-outliers", default=None, metavar="C@S",
+                    help="scale C seeded channels of X by S (heavy-tailed activations; off: the BASELINE X)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the public-API end-to-end leg (profiling runs)")
     ap.add_argument("--no-graph", action="store_true", help="issue the step's kernels one by one instead of a CUDA graph")

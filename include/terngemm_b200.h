@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define TG_ABI_VERSION 4
+#define TG_ABI_VERSION 5
 
 typedef enum {
   TG_OK = 0,
@@ -116,7 +116,10 @@ int tg_codes_check(const uint8_t* codes, int64_t count, tg_device_flags* flags, 
  * GPU-native re-encoding of any of the formats above for the dense-decode
  * tensor-core path: 2 bits per (k, n), grouped in 128-row x 1-column tiles.
  * Built from the format's own device arrays (never from a host copy).
- * Duplicate / overlapping entries set flags->corrupt (tcsc.py:105-113).        */
+ * Duplicate / overlapping entries set flags->corrupt (tcsc.py:105-113).
+ * The buffer (tg_tiles_bytes) holds the column-major tile records the decoders
+ * stream, then a row-major plane of the same 2-bit codes (16 columns per word)
+ * from which the epilogue reads W[k, n] of a row's listed outlier entries.      */
 size_t tg_tiles_bytes(int64_t K, int64_t N);
 int tg_tiles_from_dense(const int8_t* W, int64_t K, int64_t N, int64_t ldw, uint32_t* tiles,
                         tg_device_flags* flags, void* stream);
@@ -211,9 +214,12 @@ typedef struct {
  *     the limbs with exact int32 accumulation in TMEM; the epilogue recombines the
  *     limbs exactly, scales in fp64, adds the bias, rounds once to fp32 and
  *     applies PReLU.  Rows whose nonzero entries span more than a 16x
- *     max/rms dynamic range are then recomputed in the reference's exact order
- *     from `exact` (a second, usually empty, launch); with exact == NULL they
- *     keep the limb result.
+ *     max/rms dynamic range first shed their few large entries (at most 32 per
+ *     row, e.g. LLM outlier channels): prepare lists them as (k, x) pairs, the limbs
+ *     carry the rest at the rest's own scale, and the epilogue adds the listed
+ *     terms from the packed tile words in fp32.  Rows that stay wide after that
+ *     are recomputed in the reference's exact order from `exact` (inside the
+ *     epilogue); with exact == NULL they keep the limb result.
  * Bit-exact with the reference for integer-valued X; otherwise the only
  * rounding is X's 22-bit per-row grid and one final rounding (~1e-7 normwise).
  * The tiles hold only real nonzeros: the symmetric formats' dummy indices
@@ -223,6 +229,9 @@ typedef struct {
  * tg_gemm_tiles = prepare + run.                                               */
 int tg_gemm_tiles_prepare(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size_t ws_bytes,
                           tg_device_flags* flags, void* stream);
+/* Diagnostics of a prepared workspace (synchronises `stream`): stats[0] = rows left to the
+ * exact-order walk, stats[1] = rows with listed outlier entries, stats[2] = listed entries. */
+int tg_gemm_tiles_row_stats(const void* ws, size_t ws_bytes, int64_t M, int64_t K, int64_t* stats, void* stream);
 int tg_gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N,
                       const float* bias, float* Y, int64_t ldy, int use_alpha, float alpha, const tg_format_ref* exact,
                       void* ws, size_t ws_bytes, tg_device_flags* flags, void* stream);

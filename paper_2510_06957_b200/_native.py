@@ -145,6 +145,7 @@ SIGNATURES: dict[str, tuple] = {
     ),
     "tg_gemm_compressed": (_I, [_P, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _P, _SZ, _P, _P]),
     "tg_gemm_tiles_prepare": (_I, [_P, _I64, _I64, _I64, _P, _SZ, _P, _P]),
+    "tg_gemm_tiles_row_stats": (_I, [_P, _SZ, _I64, _I64, _P, _P]),
     "tg_gemm_tiles_run": (_I, [_P, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _I, _F, _P, _P, _SZ, _P, _P]),
     "tg_gemm_tiles": (_I, [_P, _I64, _I64, _I64, _P, _I64, _P, _P, _I64, _I, _F, _P, _P, _SZ, _P, _P]),
     "tg_gemm_host_workspace_bytes": (_SZ, [_I64, _I64, _I64]),
@@ -177,12 +178,13 @@ def load() -> ctypes.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        if not os.path.exists(LIB_PATH):
+        path = os.environ.get("TG_LIB_PATH") or LIB_PATH  # (A/B runs of an alternative build)
+        if not os.path.exists(path):
             raise NativeError(
                 f"{LIB_NAME} not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
                 f"or `make -C {os.path.dirname(LIB_PATH)}` (there is no CPU fallback)"
             )
-        lib = ctypes.CDLL(LIB_PATH)
+        lib = ctypes.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res

@@ -81,9 +81,14 @@ int tg_device_supported(int dev) {
 }
 
 // ------------------------------------------------------------------ tiles
+// The column-major tile records, then the same 2-bit codes as a row-major plane of equal size
+// (tg_rows_plane_kernel: the outlier terms of the epilogue read W[k, n] for 32 columns at once).
+static size_t tile_records_bytes(int64_t K, int64_t N) {
+  return size_t(ceil_div(K, 128)) * size_t(round_up(N, 128)) * 8 * sizeof(uint32_t);
+}
 size_t tg_tiles_bytes(int64_t K, int64_t N) {
   if (K < 1 || N < 1) return 0;
-  return size_t(ceil_div(K, 128)) * size_t(round_up(N, 128)) * 8 * sizeof(uint32_t);
+  return 2 * tile_records_bytes(K, N);
 }
 
 int tg_tiles_from_dense(const int8_t* W, int64_t K, int64_t N, int64_t ldw, uint32_t* tiles,
@@ -92,7 +97,8 @@ int tg_tiles_from_dense(const int8_t* W, int64_t K, int64_t N, int64_t ldw, uint
   TG_REQUIRE(ldw >= N, TG_ERR_PARAM, "ldw must be >= N");
   TG_REQUIRE(W && tiles, TG_ERR_PARAM, "null pointer");
   TG_TRY(require_device());
-  return run_pack_dense(W, K, N, ldw, tiles, flags, as_stream(stream));
+  TG_TRY(run_pack_dense(W, K, N, ldw, tiles, flags, as_stream(stream)));
+  return run_rows_plane(tiles, K, N, as_stream(stream));
 }
 
 int tg_tiles_from_tcsc(const int32_t* csp, const int32_t* rip, const int32_t* csn, const int32_t* rin, int64_t K,
@@ -101,10 +107,11 @@ int tg_tiles_from_tcsc(const int32_t* csp, const int32_t* rip, const int32_t* cs
   TG_REQUIRE(csp && csn && tiles, TG_ERR_PARAM, "null pointer");
   TG_TRY(require_device());
   cudaStream_t st = as_stream(stream);
-  cudaError_t e = cudaMemsetAsync(tiles, 0, tg_tiles_bytes(K, N), st);
+  cudaError_t e = cudaMemsetAsync(tiles, 0, tile_records_bytes(K, N), st);
   if (e != cudaSuccess) return set_cuda_error(e, "cudaMemsetAsync(tiles)");
   TG_TRY(run_pack_csc(csp, rip, N, 1, false, tiles, K, flags, st));
-  return run_pack_csc(csn, rin, N, 1, true, tiles, K, flags, st);
+  TG_TRY(run_pack_csc(csn, rin, N, 1, true, tiles, K, flags, st));
+  return run_rows_plane(tiles, K, N, st);
 }
 
 int tg_tiles_from_blocked(const int32_t* csp, const int32_t* rip, const int32_t* csn, const int32_t* rin,
@@ -114,10 +121,11 @@ int tg_tiles_from_blocked(const int32_t* csp, const int32_t* rip, const int32_t*
   TG_TRY(require_device());
   cudaStream_t st = as_stream(stream);
   const int64_t nb = ceil_div(K, B);
-  cudaError_t e = cudaMemsetAsync(tiles, 0, tg_tiles_bytes(K, N), st);
+  cudaError_t e = cudaMemsetAsync(tiles, 0, tile_records_bytes(K, N), st);
   if (e != cudaSuccess) return set_cuda_error(e, "cudaMemsetAsync(tiles)");
   TG_TRY(run_pack_csc(csp, rip, N, nb, false, tiles, K, flags, st));
-  return run_pack_csc(csn, rin, N, nb, true, tiles, K, flags, st);
+  TG_TRY(run_pack_csc(csn, rin, N, nb, true, tiles, K, flags, st));
+  return run_rows_plane(tiles, K, N, st);
 }
 
 int tg_tiles_from_interleaved_blocked(const int32_t* ai, const int32_t* ptr, int64_t K, int64_t N, int64_t B, int g,
@@ -127,9 +135,10 @@ int tg_tiles_from_interleaved_blocked(const int32_t* ai, const int32_t* ptr, int
   TG_TRY(require_device());
   cudaStream_t st = as_stream(stream);
   const int64_t nb = ceil_div(K, B);
-  cudaError_t e = cudaMemsetAsync(tiles, 0, tg_tiles_bytes(K, N), st);
+  cudaError_t e = cudaMemsetAsync(tiles, 0, tile_records_bytes(K, N), st);
   if (e != cudaSuccess) return set_cuda_error(e, "cudaMemsetAsync(tiles)");
-  return run_pack_ib(ai, ptr, N, nb, g, K, tiles, flags, st);
+  TG_TRY(run_pack_ib(ai, ptr, N, nb, g, K, tiles, flags, st));
+  return run_rows_plane(tiles, K, N, st);
 }
 
 int tg_tiles_from_symmetric(const int32_t* idx, const int32_t* ptr, int64_t K, int64_t N, int g, uint32_t* tiles,
@@ -138,16 +147,18 @@ int tg_tiles_from_symmetric(const int32_t* idx, const int32_t* ptr, int64_t K, i
   TG_REQUIRE(ptr && tiles, TG_ERR_PARAM, "null pointer");
   TG_TRY(require_device());
   cudaStream_t st = as_stream(stream);
-  cudaError_t e = cudaMemsetAsync(tiles, 0, tg_tiles_bytes(K, N), st);
+  cudaError_t e = cudaMemsetAsync(tiles, 0, tile_records_bytes(K, N), st);
   if (e != cudaSuccess) return set_cuda_error(e, "cudaMemsetAsync(tiles)");
-  return run_pack_sym(idx, ptr, N, g, K, tiles, flags, st);
+  TG_TRY(run_pack_sym(idx, ptr, N, g, K, tiles, flags, st));
+  return run_rows_plane(tiles, K, N, st);
 }
 
 int tg_tiles_from_compressed(const uint8_t* codes, int64_t K, int64_t N, uint32_t* tiles, void* stream) {
   TG_REQUIRE(K >= 1 && N >= 1, TG_ERR_PARAM, "K and N must be >= 1");
   TG_REQUIRE(codes && tiles, TG_ERR_PARAM, "null pointer");
   TG_TRY(require_device());
-  return run_pack_codes(codes, K, N, tiles, as_stream(stream));
+  TG_TRY(run_pack_codes(codes, K, N, tiles, as_stream(stream)));
+  return run_rows_plane(tiles, K, N, as_stream(stream));
 }
 
 int tg_tiles_to_dense(const uint32_t* tiles, int64_t K, int64_t N, int8_t* W, void* stream) {
@@ -173,6 +184,14 @@ int tg_gemm_tiles_prepare(const float* X, int64_t M, int64_t K, int64_t ldx, voi
   TG_REQUIRE(ws_bytes >= xsplit_bytes(M, K), TG_ERR_PARAM, "workspace too small");
   TG_TRY(require_device());
   return run_xsplit(X, M, K, ldx, ws, ws_bytes, flags, as_stream(stream));
+}
+
+int tg_gemm_tiles_row_stats(const void* ws, size_t ws_bytes, int64_t M, int64_t K, int64_t* stats, void* stream) {
+  TG_REQUIRE(M >= 1 && K >= 1, TG_ERR_PARAM, "M and K must be >= 1");
+  TG_REQUIRE(ws && stats, TG_ERR_PARAM, "null pointer");
+  TG_REQUIRE(ws_bytes >= xsplit_bytes(M, K), TG_ERR_PARAM, "workspace too small");
+  TG_TRY(require_device());
+  return xsplit_row_stats(ws, M, K, stats, as_stream(stream));
 }
 
 static int gemm_tiles_run(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* tiles, int64_t N,

@@ -21,6 +21,7 @@ struct GatherArgs;  // tg_walk.cuh
 int mma_pick_mt(int64_t M);
 size_t xsplit_bytes(int64_t M, int64_t K);
 bool xsplit_single_read(int64_t K);
+int xsplit_row_stats(const void* ws, int64_t M, int64_t K, int64_t* stats, cudaStream_t st);
 size_t mma_ws_bytes(int64_t M, int64_t K, int64_t N, int share = 1);
 int run_xsplit(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size_t ws_bytes, tg_device_flags* flags,
                cudaStream_t st);
@@ -35,6 +36,7 @@ int run_pack_ib(const int32_t* ai, const int32_t* ptr, int64_t N, int64_t nblock
 int run_peer_wait(uint32_t* sig, int world, cudaStream_t st);
 
 int run_unpack_dense(const uint32_t* tiles, int64_t K, int64_t N, int8_t* W, cudaStream_t st);
+int run_rows_plane(uint32_t* tiles, int64_t K, int64_t N, cudaStream_t st);
 
 // tg_gather.cu
 enum { GATHER_BASE = 0, GATHER_BLOCKED = 1, GATHER_IB = 2, GATHER_OPTIMAL = 3, GATHER_UNROLLED = 4 };

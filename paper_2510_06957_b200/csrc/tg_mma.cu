@@ -105,6 +105,36 @@ __device__ __forceinline__ void zero_split_counters(double* rscale, int64_t M_pa
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < kSplitCounters) c[i] = 0;
 }
+// Outlier entries of a row (LLM-style activations: a few channels tens to hundreds of times
+// the rest).  A row whose amax is more than kWideRatio x the rms of its nonzeros would leave
+// the bulk of its entries only a few bits on the 22-bit grid.  Instead of sending the whole
+// row down the exact-order walk, the X split takes the few large entries out of the limbs:
+// entries beyond kOutlierCut x rms(the rest) are listed as (k, x) pairs (at most kOutlierCap
+// per row, in ascending k), the limbs carry the rest at the rest's own scale, and the GEMM
+// epilogue adds sum_k (+-x) of the listed entries from the packed tile words (exact fp32
+// adds, a fixed order).  Rows that stay wide after kOutlierRounds rounds keep the exact walk.
+constexpr int kOutlierCap = 32;
+constexpr float kOutlierCut = 8.f;
+constexpr int kOutlierRounds = 4;
+// Tail of the prepare workspace, relative to the row scales: split-K counters, the per-row
+// outlier counts, the outlier lists.
+struct PrepTail {
+  int64_t counters, ocount, olist, end;
+};
+__host__ __device__ inline PrepTail prep_tail(int64_t M_pad) {
+  PrepTail t;
+  t.counters = ((M_pad * 8 + 255) / 256) * 256;
+  t.ocount = t.counters + int64_t(kSplitCounters) * 4;
+  t.olist = t.ocount + ((M_pad * 4 + 255) / 256) * 256;
+  t.end = t.olist + M_pad * int64_t(kOutlierCap) * 8;
+  return t;
+}
+__device__ __forceinline__ int32_t* outlier_counts(double* rscale, int64_t M_pad) {
+  return reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(rscale) + prep_tail(M_pad).ocount);
+}
+__device__ __forceinline__ int2* outlier_list(double* rscale, int64_t M_pad) {
+  return reinterpret_cast<int2*>(reinterpret_cast<uint8_t*>(rscale) + prep_tail(M_pad).olist);
+}
 constexpr int64_t XS_SMEM_MAX_K = 16384;  // rows up to 64 KB are staged in shared memory
 
 // max that propagates NaN (fmaxf drops it), so a NaN anywhere in a row makes
@@ -256,6 +286,7 @@ __global__ void __launch_bounds__(XS_THREADS) tg_xsplit_kernel(const float* __re
                                   s > kMaxScaleExp || s < -kMaxScaleExp);
     const double sc = live ? ldexp(1.0, -s) : 0.0;
     rscale[m] = is_wide ? -sc : sc;
+    outlier_counts(rscale, M_pad)[m] = 0;  // (long rows: no outlier extraction, wide rows take the exact walk)
   }
 }
 
@@ -264,8 +295,15 @@ __global__ void __launch_bounds__(XS_THREADS) tg_xsplit_kernel(const float* __re
 // converted from registers.  Digits: with |v| < 2^22, u = v + 0x808080 lies in
 // [0, 2^24) and byte i of u, minus 128, is the i-th balanced base-256 digit of v
 // (the same digits as limb_digits); as int8 that is byte ^ 0x80.
+// CTAs per SM the register allocation must allow (the row lives in EPT registers; about 48
+// more cover the reductions and the outlier rounds): the split is a streaming kernel and
+// wants bytes in flight.
+constexpr int xs_min_blocks(int threads, int ept) {
+  const int b = 65536 / (threads * (48 + 2 * ept));
+  return b < 1 ? 1 : (b > 4 ? 4 : b);
+}
 template <int THREADS, int EPT>
-__global__ void __launch_bounds__(THREADS) tg_xsplit_reg_kernel(const float* __restrict__ X, int64_t M, int64_t K,
+__global__ void __launch_bounds__(THREADS, xs_min_blocks(THREADS, EPT)) tg_xsplit_reg_kernel(const float* __restrict__ X, int64_t M, int64_t K,
                                                                 int64_t ldx, int8_t* __restrict__ limbs,
                                                                 double* __restrict__ rscale, int64_t M_pad,
                                                                 int64_t K_pad, tg_device_flags* __restrict__ flags) {
@@ -274,7 +312,7 @@ __global__ void __launch_bounds__(THREADS) tg_xsplit_reg_kernel(const float* __r
   __shared__ float red_f[NW];
   __shared__ double red_d[NW];
   __shared__ int red_i[NW];
-  __shared__ int red_b[2];
+  __shared__ int red_j[NW];
   grid_dep_launch();  // the MMA kernel may start its prologue (it waits before reading our output)
   zero_split_counters(rscale, M_pad);
   if (threadIdx.x == 0) TG_GT(0);
@@ -293,6 +331,35 @@ __global__ void __launch_bounds__(THREADS) tg_xsplit_reg_kernel(const float* __r
 #pragma unroll
     for (int j = 0; j < EPT; ++j) x[j] = (in && k0 + j < K) ? __ldg(grow + k0 + j) : 0.f;
   }
+  const int w = threadIdx.x >> 5;
+  // block-wide (max, sum, sum, sum) of (float, double, int, int); every thread gets the result
+  auto reduce4 = [&](float& a, double& d, int& i, int& j2) {
+    for (int o = 16; o; o >>= 1) {
+      a = fmax_nan(a, __shfl_xor_sync(0xffffffffu, a, o));
+      d += __shfl_xor_sync(0xffffffffu, d, o);
+      i += __shfl_xor_sync(0xffffffffu, i, o);
+      j2 += __shfl_xor_sync(0xffffffffu, j2, o);
+    }
+    __syncthreads();  // (the previous round's readers are done with the arrays)
+    if ((threadIdx.x & 31) == 0) {
+      red_f[w] = a;
+      red_d[w] = d;
+      red_i[w] = i;
+      red_j[w] = j2;
+    }
+    __syncthreads();
+    a = red_f[0];
+    d = red_d[0];
+    i = red_i[0];
+    j2 = red_j[0];
+#pragma unroll
+    for (int q = 1; q < NW; ++q) {
+      a = fmax_nan(a, red_f[q]);
+      d += red_d[q];
+      i += red_i[q];
+      j2 += red_j[q];
+    }
+  };
   float amax = 0.f;
   double s2 = 0.0;
   int nz = 0;
@@ -307,13 +374,11 @@ __global__ void __launch_bounds__(THREADS) tg_xsplit_reg_kernel(const float* __r
     s2 += __shfl_xor_sync(0xffffffffu, s2, o);
     nz += __shfl_xor_sync(0xffffffffu, nz, o);
   }
-  const int w = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) {
     red_f[w] = amax;
     red_d[w] = s2;
     red_i[w] = nz;
   }
-  if (threadIdx.x == 0) red_b[0] = red_b[1] = 0;  // the big-entry count and the warp arrivals
   __syncthreads();
   amax = red_f[0];
   s2 = red_d[0];
@@ -326,20 +391,115 @@ __global__ void __launch_bounds__(THREADS) tg_xsplit_reg_kernel(const float* __r
   }
   const bool finite = amax <= 3.402823466e38f;  // false for inf / nan
   const bool live = in && amax > 0.f && finite;
+  if (in && !finite && threadIdx.x == 0 && flags) atomicOr(&flags->bad_input, 4);
+
+  // block-wide sum of an int; every thread gets the result
+  auto reduce_int = [&](int v) {
+    v = __reduce_add_sync(0xffffffffu, v);
+    __syncthreads();  // (the previous round's readers are done with the array)
+    if ((threadIdx.x & 31) == 0) red_i[w] = v;
+    __syncthreads();
+    v = red_i[0];
+#pragma unroll
+    for (int q = 1; q < NW; ++q) v += red_i[q];
+    return v;
+  };
+  // The two "wide" rules: amax / rms(nonzeros) > kWideRatio (nz amax^2 > kWideRatio^2 sum x^2),
+  // or fewer than 1 / kWideFrac of the nonzeros within kWideRatio of amax.
+  const double wide2 = double(kWideRatio) * double(kWideRatio);
+  int big = 0;
+#pragma unroll
+  for (int j = 0; j < EPT; ++j) big += (fabsf(x[j]) * kWideRatio >= amax && x[j] != 0.f) ? 1 : 0;
+  big = reduce_int(big);
+  bool wide = live && (double(nz) * double(amax) * double(amax) > wide2 * s2 || big * kWideFrac < nz);
+
+  // Outlier extraction (every branch below is block-uniform): a wide row sheds the entries
+  // beyond kOutlierCut x rms(rest), round by round, until the rest passes both rules.
+  static_assert(EPT <= 32, "the outlier mask is one word per thread");
+  uint32_t omask = 0;  // bit j: x[j] is listed instead of entering the limbs
+  int n_out = 0;
+  if (wide) {
+    float amax_r = amax;
+    double s2_r = s2;
+    int nz_r = nz;
+    bool ok = false;
+#pragma unroll 1
+    for (int round = 0; round < kOutlierRounds; ++round) {
+      const float cut = kOutlierCut * float(sqrt(s2_r / double(nz_r)));
+      float am = 0.f, ssf = 0.f;  // (a thread's <= 32 squares in fp32, scaled by 1 / cut^2: no overflow)
+      const float icut = 1.f / cut;
+      int cnt = 0;
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) {
+        const float a = fabsf(x[j]);
+        if (a > cut) {
+          omask |= 1u << j;
+        } else if (!((omask >> j) & 1u)) {
+          am = fmaxf(am, a);
+          const float t = a * icut;
+          ssf = fmaf(t, t, ssf);
+          cnt += a != 0.f;
+        }
+      }
+      double ss = double(ssf) * double(cut) * double(cut);
+      int no = __popc(omask);
+      reduce4(am, ss, cnt, no);
+      amax_r = am;
+      s2_r = ss;
+      nz_r = cnt;
+      n_out = no;
+      if (n_out > kOutlierCap || nz_r == 0) break;
+      if (double(nz_r) * double(amax_r) * double(amax_r) > wide2 * s2_r) continue;  // still wide: next round
+      int big_r = 0;
+#pragma unroll
+      for (int j = 0; j < EPT; ++j)
+        big_r += (!((omask >> j) & 1u) && x[j] != 0.f && fabsf(x[j]) * kWideRatio >= amax_r) ? 1 : 0;
+      big_r = reduce_int(big_r);
+      if (big_r * kWideFrac >= nz_r) {  // the rest passes both rules
+        ok = true;
+        break;
+      }
+    }
+    if (ok) {
+      // list the outliers in ascending k: exclusive prefix of the per-thread counts
+      const int mine = __popc(omask);
+      int incl = mine;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((threadIdx.x & 31) >= o) incl += t;
+      }
+      __syncthreads();
+      if ((threadIdx.x & 31) == 31) red_i[w] = incl;
+      __syncthreads();
+      int pos = incl - mine;
+      for (int q = 0; q < w; ++q) pos += red_i[q];
+      int2* lst = outlier_list(rscale, M_pad) + m * kOutlierCap;
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) {
+        if ((omask >> j) & 1u) {
+          lst[pos++] = make_int2(int(k0) + j, __float_as_int(x[j]));
+          x[j] = 0.f;  // the limbs see the rest only
+        }
+      }
+      amax = amax_r;
+      wide = false;
+    } else {
+      n_out = 0;
+    }
+  }
   int s = 0;
   if (live) {
     int e;
     frexpf(amax, &e);  // amax < 2^e
     s = 22 - e;        // |x * 2^s| < 2^22
-  } else if (in && !finite && threadIdx.x == 0 && flags) {
-    atomicOr(&flags->bad_input, 4);
   }
-  // Entries within kWideRatio of amax: counted after the limbs are stored (no second
-  // barrier before the stores): each warp adds its count, the last warp to arrive writes
-  // the row's scale and wide flag.
-  int big = 0;
-#pragma unroll
-  for (int j = 0; j < EPT; ++j) big += (fabsf(x[j]) * kWideRatio >= amax && x[j] != 0.f) ? 1 : 0;
+  if (threadIdx.x == 0) {
+    // (a scale outside the epilogue's fp32 range also sends the row to the exact walk)
+    const bool is_wide = wide || (live && (s > kMaxScaleExp || s < -kMaxScaleExp));
+    const double sc = live ? ldexp(1.0, -s) : 0.0;
+    rscale[m] = is_wide ? -sc : sc;
+    outlier_counts(rscale, M_pad)[m] = is_wide ? 0 : n_out;
+  }
   if (k0 < K_pad) {
     // x * 2^s as two exact power-of-two multiplies (2^s alone may exceed the float range)
     const int s_a = s > 126 ? 126 : (s < -126 ? -126 : s);
@@ -377,20 +537,7 @@ __global__ void __launch_bounds__(THREADS) tg_xsplit_reg_kernel(const float* __r
       }
     }
   }
-  big = __reduce_add_sync(0xffffffffu, big);
-  if ((threadIdx.x & 31) == 0) {
-    atomicAdd(&red_b[0], big);
-    __threadfence_block();
-    if (atomicAdd(&red_b[1], 1) == NW - 1) {  // last warp: every count is in
-      big = atomicAdd(&red_b[0], 0);
-      // amax / rms(nonzeros) > kWideRatio  <=>  nz * amax^2 > kWideRatio^2 * sum x^2; few entries near amax
-      const bool is_wide = live && (double(nz) * double(amax) * double(amax) > double(kWideRatio * kWideRatio) * s2 ||
-                                    big * kWideFrac < nz || s > kMaxScaleExp || s < -kMaxScaleExp);
-      const double sc = live ? ldexp(1.0, -s) : 0.0;
-      rscale[m] = is_wide ? -sc : sc;
-      TG_GT(1);
-    }
-  }
+  if (threadIdx.x == 0) TG_GT(1);
 }
 
 // ------------------------------------------------------------------ decode
@@ -414,6 +561,7 @@ __device__ __forceinline__ uint4 decode_word(uint32_t w) {
 // ------------------------------------------------------------------ MMA
 struct MmaParams {
   const uint32_t* tiles;   // [KC][N_pad][8] packed ternary words
+  const uint32_t* wrows;   // [KC * 128][N_pad / 16] the same codes row-major, 16 columns per word (outlier terms)
   const double* rscale;    // [M_pad], < 0 marks a wide row
   const float* bias;       // [N] or null
   float* Y;
@@ -443,6 +591,9 @@ struct MmaParams {
   // host Y (device-mapped), so no copy-engine D2H follows the GEMM; null: off
   float* yh;
   int64_t ldyh;
+  // outlier entries the X split kept out of the limbs: counts [M_pad], lists [M_pad][kOutlierCap] of (k, x bits)
+  const int32_t* ocount;
+  const int2* olist;
 };
 
 // One Y row segment to every other rank's full Y (plain st.global over NVLink).
@@ -533,6 +684,8 @@ struct EmitCtx {
   uint32_t sc_addr;  // smem address of the float scale of row m_first
   float bf;
   uint32_t wide_bits;
+  uint32_t out_bits;  // rows (of the 16) with listed outlier entries
+  const float* corr;  // their summed outlier terms (16 floats, 0 for the other rows)
   int m_first;
   int nlive;   // rows of this chunk inside Y (counting, fp64 fall-back)
   int nvalid;  // rows to store (16 into the smem tile: the TMA store clips rows >= M)
@@ -556,6 +709,11 @@ __device__ __forceinline__ void load_scales(uint32_t addr, float4 (&sc)[16]) {
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                  : "=f"(sc[j].x), "=f"(sc[j].y), "=f"(sc[j].z), "=f"(sc[j].w)
                  : "r"(addr + 16u * j));
+}
+// (2^-s of 16 consecutive rows from either form: `stride` bytes between rows)
+__device__ __forceinline__ void load_scales(uint32_t addr, float (&sc)[16], uint32_t stride) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(sc[j]) : "r"(addr + stride * j));
 }
 __device__ __forceinline__ void load_scales(uint32_t addr, float (&sc)[16]) {
 #pragma unroll
@@ -693,13 +851,53 @@ __device__ __forceinline__ void host_copy_tile(const MmaParams& p, const float* 
   }
 }
 
+// sum over row m's listed outlier entries of W[k, n] * x (the list is in ascending k: a fixed
+// order).  The list reads are warp-uniform, and W[k, n] comes from the row-major 2-bit plane
+// behind the tiles (16 columns per word): the 32 columns of a warp share one 32-byte sector
+// per entry (the column-major tile records would cost one sector per lane).
+__device__ __noinline__ float outlier_sum(const MmaParams& p, int m, int n) {
+  const int cnt = __ldg(p.ocount + m);
+  const int2* lst = p.olist + int64_t(m) * kOutlierCap;
+  const uint32_t* col = p.wrows + (n >> 4);
+  const int64_t kstride = p.N_pad >> 4;
+  const int sh = 2 * (n & 15);
+  float acc = 0.f;
+#pragma unroll 1
+  for (int i0 = 0; i0 < cnt; i0 += 8) {
+    int2 e[8];
+    uint32_t w[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) e[t] = i0 + t < cnt ? __ldg(lst + i0 + t) : make_int2(0, 0);  // (k = 0, x = 0: adds 0)
+#pragma unroll
+    for (int t = 0; t < 8; ++t) w[t] = __ldg(col + int64_t(e[t].x) * kstride);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const uint32_t code = (w[t] >> sh) & 3u;
+      const float x = __int_as_float(e[t].y);
+      acc += code == 1u ? x : (code == 3u ? -x : 0.f);
+    }
+  }
+  return acc;
+}
+
 // from the three limb sums of a finished accumulator (TMEM)
 template <bool COMPACT>
 __device__ __forceinline__ void emit16_limbs(const uint32_t (&r0)[16], const uint32_t (&r1)[16],
                                              const uint32_t (&r2)[16], const EmitCtx& e, const MmaParams& p,
                                              unsigned long long& npos, bool& bad) {
   float v[16];
-  if constexpr (COMPACT) {
+  if (e.out_bits && e.n_ok) {
+    // rows with listed outliers: y = limbs + (b + the row's outlier terms); the terms were
+    // summed while the unit's MMAs ran and wait in local memory (e.corr)
+    float sc[16];
+    load_scales(e.sc_addr, sc, COMPACT ? 4u : 16u);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float s0 = sc[j], s1 = s0 * 256.f, s2 = s0 * 65536.f;
+      v[j] = __fmaf_rn(float(int(r0[j])), s2,
+                       __fmaf_rn(float(int(r1[j])), s1, __fmaf_rn(float(int(r2[j])), s0, e.bf + e.corr[j])));
+    }
+  } else if constexpr (COMPACT) {
     float sc[16];
     load_scales(e.sc_addr, sc);
 #pragma unroll
@@ -926,6 +1124,9 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           if (c < nch) {
+            // (two 16-byte loads at a 32-byte lane stride: a 2-way bank conflict.  Swapping the
+            // halves on lanes 4-7 of every phase removes it but costs selects on the decoders'
+            // critical path: cfg4 +1.7 us, cfg2 neutral, profiles/r02_v3/ab_halfswap.txt)
             const uint32_t src = smem_u32(sP + sp * C::P_BYTES + c * C::P_CHUNK) + row * 32u;
             w[c][0] = lds128(src);
             w[c][1] = lds128(src + 16u);
@@ -979,6 +1180,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
     constexpr bool COMPACT = C::DEC_GROUPS > 1;     // (the 608-thread kernels: see load_scales)
     float* sc_s = reinterpret_cast<float*>(rs_s);  // [80] row scales of the unit (x4 when !COMPACT)
     uint32_t* wmask = reinterpret_cast<uint32_t*>(rs_s + 160);  // [4] wide-row bits of the unit (after 80 float4)
+    uint32_t* omask = reinterpret_cast<uint32_t*>(rs_s + 163);  // [4] rows with listed outliers (after the PReLU count)
     bool any_bad = false;
     unsigned long long npos = 0;
     uint32_t lu = 0;
@@ -1004,9 +1206,28 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
               make_float4(float(a), float(a * 256.0), float(a * 65536.0), float(a * 16777216.0));
         }
         const uint32_t wbits = __ballot_sync(0xffffffffu, rs < 0.0);
-        if (lane == 0 && (et >> 5) < 4) wmask[et >> 5] = wbits;
+        const uint32_t obits = __ballot_sync(0xffffffffu, et < MT && __ldcg(p.ocount + m0 + et) > 0);
+        if (lane == 0 && (et >> 5) < 4) {
+          wmask[et >> 5] = wbits;
+          omask[et >> 5] = obits;
+        }
       }
       named_bar_sync(1, ET);
+      // Outlier terms of this thread's rows (the X split listed the entries it kept out of the
+      // limbs): summed here, while the unit's MMAs run, so the lookups hide behind them.
+      float corr[16 * ((MT + 31) / 32)];
+      auto fill_corr = [&]() {
+        if (!n_ok) return;
+#pragma unroll 1
+        for (int mm = 16 * half; mm < MT; mm += 32) {
+          const uint32_t bits = (omask[mm >> 5] >> (mm & 31)) & 0xFFFFu;
+          if (!bits) continue;
+#pragma unroll 1
+          for (int j = 0; j < 16; ++j)
+            corr[(mm >> 5) * 16 + j] = ((bits >> j) & 1u) ? outlier_sum(p, m0 + mm + j, n) : 0.f;
+        }
+      };
+      if (p.splits == 1) fill_corr();
       mbar_wait(&tfull[acc], use & 1);
       if (et == 0) TG_STAMP(7, 2 + 2 * lu);
       tc_fence_after();
@@ -1017,6 +1238,8 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
         e.sc_addr = rs_addr + (COMPACT ? 4u : 16u) * uint32_t(mm);
         e.bf = bf;
         e.wide_bits = (wmask[mm >> 5] >> (mm & 31)) & 0xFFFFu;
+        e.out_bits = (omask[mm >> 5] >> (mm & 31)) & 0xFFFFu;
+        e.corr = corr + (mm >> 5) * 16;
         e.m_first = m0 + mm;
         e.nlive = min(16, p.M - (m0 + mm));
         e.nvalid = e.nlive;
@@ -1080,6 +1303,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
         final_writer = *last_flag != 0;
         if (final_writer) {
           __threadfence();
+          fill_corr();
 #pragma unroll 1
           for (int j0 = 16 * half; j0 < MT; j0 += 32) {
             // 16 independent rows per batch so the L2 reads of the partials overlap;
@@ -1481,7 +1705,7 @@ static int max_clusters_for(int64_t mt, int cs) {
 struct SplitLayout {
   int64_t mt, M_pad, K_pad, N_pad, KC, MB, NB, NBG;
   int splits, cs, clusters;
-  size_t off_rscale, off_counters, off_part, total_prepare, total;
+  size_t off_rscale, off_counters, off_ocount, off_olist, off_part, total_prepare, total;
 };
 
 // `share` > 1: this GEMM runs beside share - 1 others (host streaming's row chunks on
@@ -1504,8 +1728,11 @@ static SplitLayout split_layout(int64_t M, int64_t K, int64_t N, int share = 1) 
     if (N > 0) L.splits = int(std::max<int64_t>(1, std::min<int64_t>(atoi(env), ceil_div(L.KC, 2))));
   if (L.MB * L.NB > kSplitCounters) L.splits = 1;  // the split zeroes kSplitCounters counters
   L.off_rscale = size_t(round_up(3 * L.M_pad * L.K_pad, 256));
-  L.off_counters = L.off_rscale + size_t(round_up(L.M_pad * int64_t(sizeof(double)), 256));
-  L.total_prepare = L.off_counters + size_t(kSplitCounters) * 4;
+  const PrepTail pt = prep_tail(L.M_pad);
+  L.off_counters = L.off_rscale + size_t(pt.counters);
+  L.off_ocount = L.off_rscale + size_t(pt.ocount);
+  L.off_olist = L.off_rscale + size_t(pt.olist);
+  L.total_prepare = size_t(round_up(int64_t(L.off_rscale) + pt.end, 256));
   L.off_part = L.total_prepare;
   L.total = L.splits > 1 ? L.off_part + size_t(L.splits) * 3 * size_t(L.M_pad) * size_t(L.N_pad) * 4
                          : L.total_prepare;
@@ -1518,6 +1745,33 @@ size_t xsplit_bytes(int64_t M, int64_t K) { return split_layout(M, K, 0).total_p
 // from host memory) would double the transfer
 bool xsplit_single_read(int64_t K) { return split_layout(1, K, 0).K_pad <= 1024 * 32 || K <= XS_SMEM_MAX_K; }
 size_t mma_ws_bytes(int64_t M, int64_t K, int64_t N, int share) { return split_layout(M, K, N, share).total; }
+
+// rows left to the exact walk / rows with listed outliers / listed entries of a prepared workspace
+int xsplit_row_stats(const void* ws, int64_t M, int64_t K, int64_t* stats, cudaStream_t st) {
+  const SplitLayout L = split_layout(M, K, 0);
+  const uint8_t* base = static_cast<const uint8_t*>(ws);
+  double* rs = static_cast<double*>(malloc(size_t(M) * sizeof(double)));
+  int32_t* oc = static_cast<int32_t*>(malloc(size_t(M) * sizeof(int32_t)));
+  if (!rs || !oc) {
+    free(rs);
+    free(oc);
+    return set_error(TG_ERR_PARAM, "out of host memory");
+  }
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = cudaMemcpy(rs, base + L.off_rscale, size_t(M) * sizeof(double), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(oc, base + L.off_ocount, size_t(M) * sizeof(int32_t), cudaMemcpyDeviceToHost);
+  stats[0] = stats[1] = stats[2] = 0;
+  if (e == cudaSuccess) {
+    for (int64_t m = 0; m < M; ++m) {
+      stats[0] += rs[m] < 0.0;
+      stats[1] += oc[m] > 0;
+      stats[2] += oc[m];
+    }
+  }
+  free(rs);
+  free(oc);
+  return e == cudaSuccess ? TG_OK : set_cuda_error(e, "xsplit_row_stats");
+}
 
 int run_xsplit(const float* X, int64_t M, int64_t K, int64_t ldx, void* ws, size_t ws_bytes, tg_device_flags* flags,
                cudaStream_t st) {
@@ -1647,6 +1901,7 @@ int run_mma(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* t
   MmaParams p{};
   p.tma_y = tma_y;
   p.tiles = tiles;
+  p.wrows = tiles + size_t(L.KC) * size_t(L.N_pad) * 8;
   p.rscale = reinterpret_cast<const double*>(base + L.off_rscale);
   p.bias = bias;
   p.Y = Y;
@@ -1676,6 +1931,8 @@ int run_mma(const float* X, int64_t M, int64_t K, int64_t ldx, const uint32_t* t
   }
   p.yh = yh;
   p.ldyh = ldyh;
+  p.ocount = reinterpret_cast<const int32_t*>(base + L.off_ocount);
+  p.olist = reinterpret_cast<const int2*>(base + L.off_olist);
   if (sc) {
     p.ypeers = sc->y_peers;
     p.speers = sc->sig_peers;
@@ -1738,6 +1995,37 @@ int run_pack_ib(const int32_t* ai, const int32_t* ptr, int64_t N, int64_t nblock
 }  // namespace tg
 
 namespace tg {
+
+// Tiles -> the row-major 2-bit plane stored right behind them: rows[k][N_pad / 16], column n of
+// row k at bits 2 (n % 16) of word n / 16 (1: +1, 3: -1, 0: zero).  One thread per output word.
+__global__ void tg_rows_plane_kernel(const uint32_t* __restrict__ tiles, int64_t KC, int64_t N_pad,
+                                     uint32_t* __restrict__ rows) {
+  const int64_t wpr = N_pad >> 4;
+  const int64_t total = KC * 128 * wpr;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t k = idx / wpr, j16 = idx % wpr;
+    const int64_t kc = k >> 7;
+    const int c = int((k >> 4) & 7), j = int(k & 15);
+    const int bit = 8 * (j & 3) + 2 * (j >> 2);
+    uint32_t out = 0;
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const uint32_t w = __ldg(tiles + (kc * N_pad + j16 * 16 + t) * 8 + c);
+      out |= ((w >> bit) & 3u) << (2 * t);
+    }
+    rows[idx] = out;
+  }
+}
+
+int run_rows_plane(uint32_t* tiles, int64_t K, int64_t N, cudaStream_t st) {
+  const int64_t KC = round_up(K, 128) / 128;
+  const int64_t N_pad = round_up(N, 128);
+  const int64_t total = KC * 128 * (N_pad >> 4);
+  const unsigned blocks = unsigned(std::min<int64_t>((total + 255) / 256, 148 * 32));
+  tg_rows_plane_kernel<<<blocks, 256, 0, st>>>(tiles, KC, N_pad, tiles + KC * N_pad * 8);
+  return check_launch("tg_rows_plane_kernel");
+}
 
 // Tiles -> dense int8 W (K x N, ld = N).  One thread per (k, n).
 __global__ void tg_unpack_dense_kernel(const uint32_t* __restrict__ tiles, int64_t K, int64_t N, int64_t N_pad,

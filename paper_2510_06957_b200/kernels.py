@@ -412,6 +412,20 @@ class GemmRunner:
                      _p(f.device("col_segment_ptr")), N, b, y, self.ldy, order, self.use_alpha, self.alpha, _p(ws),
                      ws.numel(), fl, st)
 
+    def row_stats(self) -> dict:
+        """Diagnostics of the tensor-core path's X split (run on the pinned workspace):
+        how many rows went to the exact-order walk, how many shed outlier entries, and how
+        many entries were listed.  Synchronises."""
+        if self.method != "mma":
+            raise ParameterError("row_stats describes the tensor-core path")
+        if self._ws is None:
+            self.pin_workspace()
+        self.launch(stage="prepare")
+        out = (ctypes.c_int64 * 3)()
+        nat.call("tg_gemm_tiles_row_stats", _p(self._ws), self._ws.numel(), self.M, self.K, out,
+                 torch.cuda.current_stream().cuda_stream)
+        return {"exact_rows": int(out[0]), "outlier_rows": int(out[1]), "outlier_entries": int(out[2])}
+
     def capture(self, warmup: bool = True) -> "torch.cuda.CUDAGraph":
         """Capture ``launch()`` (X split + tile MMA, or the gather walk) into a CUDA
         graph: one host launch per replay, no host gaps between the kernels

@@ -423,8 +423,9 @@ def test_wide_dynamic_range_rows_take_exact_fixup(tg):
     ref = orc.gemm_vectorized_optimal(orc.pad_input(X), ref_t, b, 0.25)
     y, ops = tg.gemm_vectorized_optimal(tg.pad_input(X), t, b, 0.25, method="mma", counted=True)
     y = y.values
-    for r in (3, 7, 11):
-        assert np.array_equal(y[r], ref[r]), r
+    # row 7's scale leaves the epilogue's range: exact walk, bit-identical.  Rows 3 and 11 shed
+    # their one large entry instead (tests/test_gpu_outliers.py) and meet the bars below.
+    assert np.array_equal(y[7], ref[7])
     _assert_tol(y, X, W, b, 0.25)
     ref_lin = orc.oracle_gemm(X, W, b)
     assert abs(ops.mults - int((ref_lin <= 0).sum())) <= 2

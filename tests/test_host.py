@@ -175,9 +175,9 @@ def test_c_abi_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
     assert set(names) == set(_native.SIGNATURES), set(names) ^ set(_native.SIGNATURES)
     L = _native.load()
-    assert L.tg_abi_version() == 4
+    assert L.tg_abi_version() == 5
     # pure size queries need no device
-    assert L.tg_tiles_bytes(4096, 4096) == 32 * 4096 * 8 * 4
+    assert L.tg_tiles_bytes(4096, 4096) == 2 * 32 * 4096 * 8 * 4  # tile records + the row-major plane
     assert L.tg_build_workspace_bytes(4096, 4096, 4096) > 0
     assert L.tg_gemm_workspace_bytes(256, 4096, 4096) >= 3 * 256 * 4096
 
