@@ -19,7 +19,7 @@ from .errors import CorruptionError, ParameterError
 LIB_NAME = "libterngemm_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 # developer override (e.g. the clock64-instrumented libterngemm_b200_trace.so); never set in production
-LIB_PATH = os.environ.get("TG_LIB_PATH", LIB_PATH)
+LIB_PATH = os.environ.get("TG_LIB_PATH") or LIB_PATH
 
 TG_OK = 0
 TG_ERR_PARAM = 1
@@ -178,7 +178,7 @@ def load() -> ctypes.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        path = os.environ.get("TG_LIB_PATH") or LIB_PATH  # (A/B runs of an alternative build)
+        path = LIB_PATH
         if not os.path.exists(path):
             raise NativeError(
                 f"{LIB_NAME} not built; run `python -c 'import __graft_entry__ as g; g.build()'` "

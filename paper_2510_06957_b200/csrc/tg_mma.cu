@@ -299,6 +299,7 @@ __global__ void __launch_bounds__(XS_THREADS) tg_xsplit_kernel(const float* __re
 // more cover the reductions and the outlier rounds): the split is a streaming kernel and
 // wants bytes in flight.
 constexpr int xs_min_blocks(int threads, int ept) {
+  if (threads >= 512) return 1;  // (the wide CTAs serve few-row inputs: occupancy is not their bound)
   const int b = 65536 / (threads * (48 + 2 * ept));
   return b < 1 ? 1 : (b > 4 ? 4 : b);
 }
@@ -313,6 +314,7 @@ __global__ void __launch_bounds__(THREADS, xs_min_blocks(THREADS, EPT)) tg_xspli
   __shared__ double red_d[NW];
   __shared__ int red_i[NW];
   __shared__ int red_j[NW];
+  __shared__ float red_g[NW];
   grid_dep_launch();  // the MMA kernel may start its prologue (it waits before reading our output)
   zero_split_counters(rscale, M_pad);
   if (threadIdx.x == 0) TG_GT(0);
@@ -332,10 +334,11 @@ __global__ void __launch_bounds__(THREADS, xs_min_blocks(THREADS, EPT)) tg_xspli
     for (int j = 0; j < EPT; ++j) x[j] = (in && k0 + j < K) ? __ldg(grow + k0 + j) : 0.f;
   }
   const int w = threadIdx.x >> 5;
-  // block-wide (max, sum, sum, sum) of (float, double, int, int); every thread gets the result
-  auto reduce4 = [&](float& a, double& d, int& i, int& j2) {
+  // block-wide (max, sum, sum, sum, sum) of (float, float, double, int, int); every thread gets the result
+  auto reduce5 = [&](float& a, float& g, double& d, int& i, int& j2) {
     for (int o = 16; o; o >>= 1) {
       a = fmax_nan(a, __shfl_xor_sync(0xffffffffu, a, o));
+      g += __shfl_xor_sync(0xffffffffu, g, o);
       d += __shfl_xor_sync(0xffffffffu, d, o);
       i += __shfl_xor_sync(0xffffffffu, i, o);
       j2 += __shfl_xor_sync(0xffffffffu, j2, o);
@@ -343,49 +346,57 @@ __global__ void __launch_bounds__(THREADS, xs_min_blocks(THREADS, EPT)) tg_xspli
     __syncthreads();  // (the previous round's readers are done with the arrays)
     if ((threadIdx.x & 31) == 0) {
       red_f[w] = a;
+      red_g[w] = g;
       red_d[w] = d;
       red_i[w] = i;
       red_j[w] = j2;
     }
     __syncthreads();
     a = red_f[0];
+    g = red_g[0];
     d = red_d[0];
     i = red_i[0];
     j2 = red_j[0];
 #pragma unroll
     for (int q = 1; q < NW; ++q) {
       a = fmax_nan(a, red_f[q]);
+      g += red_g[q];
       d += red_d[q];
       i += red_i[q];
       j2 += red_j[q];
     }
   };
-  float amax = 0.f;
+  float amax = 0.f, s1 = 0.f;  // (s1 = sum |x| may overflow to inf for huge rows: the cut then falls back to the rms)
   double s2 = 0.0;
   int nz = 0;
 #pragma unroll
   for (int j = 0; j < EPT; ++j) {
     amax = fmax_nan(amax, fabsf(x[j]));
+    s1 += fabsf(x[j]);
     s2 = fma(double(x[j]), double(x[j]), s2);
     nz += x[j] != 0.f;
   }
   for (int o = 16; o; o >>= 1) {
     amax = fmax_nan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
     s2 += __shfl_xor_sync(0xffffffffu, s2, o);
     nz += __shfl_xor_sync(0xffffffffu, nz, o);
   }
   if ((threadIdx.x & 31) == 0) {
     red_f[w] = amax;
+    red_g[w] = s1;
     red_d[w] = s2;
     red_i[w] = nz;
   }
   __syncthreads();
   amax = red_f[0];
+  s1 = red_g[0];
   s2 = red_d[0];
   nz = red_i[0];
 #pragma unroll
   for (int i = 1; i < NW; ++i) {
     amax = fmax_nan(amax, red_f[i]);
+    s1 += red_g[i];
     s2 += red_d[i];
     nz += red_i[i];
   }
@@ -423,10 +434,14 @@ __global__ void __launch_bounds__(THREADS, xs_min_blocks(THREADS, EPT)) tg_xspli
     double s2_r = s2;
     int nz_r = nz;
     bool ok = false;
+    // The cut is kOutlierCut x the scale of the rest: its rms, or 1.25 x its mean |x| (the
+    // ratio of the two for a normal bulk) when that is smaller -- a few huge entries inflate the
+    // rms far more than the mean, so the mean-based cut usually clears the row in one round.
+    float s1_r = s1;  // sum |x| over the current rest
 #pragma unroll 1
     for (int round = 0; round < kOutlierRounds; ++round) {
-      const float cut = kOutlierCut * float(sqrt(s2_r / double(nz_r)));
-      float am = 0.f, ssf = 0.f;  // (a thread's <= 32 squares in fp32, scaled by 1 / cut^2: no overflow)
+      const float cut = kOutlierCut * fminf(float(sqrt(s2_r / double(nz_r))), 1.25f * s1_r / float(nz_r));
+      float am = 0.f, ssf = 0.f, s1f = 0.f;  // (a thread's <= 32 terms in fp32, scaled by the cut: no overflow)
       const float icut = 1.f / cut;
       int cnt = 0;
 #pragma unroll
@@ -438,13 +453,15 @@ __global__ void __launch_bounds__(THREADS, xs_min_blocks(THREADS, EPT)) tg_xspli
           am = fmaxf(am, a);
           const float t = a * icut;
           ssf = fmaf(t, t, ssf);
+          s1f += t;
           cnt += a != 0.f;
         }
       }
       double ss = double(ssf) * double(cut) * double(cut);
       int no = __popc(omask);
-      reduce4(am, ss, cnt, no);
+      reduce5(am, s1f, ss, cnt, no);
       amax_r = am;
+      s1_r = s1f * cut;
       s2_r = ss;
       nz_r = cnt;
       n_out = no;
@@ -851,33 +868,65 @@ __device__ __forceinline__ void host_copy_tile(const MmaParams& p, const float* 
   }
 }
 
-// sum over row m's listed outlier entries of W[k, n] * x (the list is in ascending k: a fixed
-// order).  The list reads are warp-uniform, and W[k, n] comes from the row-major 2-bit plane
-// behind the tiles (16 columns per word): the 32 columns of a warp share one 32-byte sector
-// per entry (the column-major tile records would cost one sector per lane).
-__device__ __noinline__ float outlier_sum(const MmaParams& p, int m, int n) {
-  const int cnt = __ldg(p.ocount + m);
-  const int2* lst = p.olist + int64_t(m) * kOutlierCap;
-  const uint32_t* col = p.wrows + (n >> 4);
-  const int64_t kstride = p.N_pad >> 4;
+// Outlier terms of 16 consecutive rows for this lane's column n: corr[r] = sum over row
+// (m_first + r)'s listed entries of W[k, n] * x, in list order (ascending k: a fixed order).
+// The whole warp cooperates, in two memory round trips per batch of 16 entries of every row:
+//   1. lane l loads entries i0 + 2t + l / 16 (t < 8) of row l % 16, together with the row's count;
+//   2. lane l loads, for each of ITS entries, the two words of the row-major 2-bit plane behind
+//      the tiles that hold W[k, .] for the warp's 32 columns (16 columns per word) -- the 256
+//      (row, entry) pairs of the batch are all in flight at once;
+// then every pair's (x, word pair) is broadcast by shuffle and each lane adds its column's term.
+// (One lane per column walking its rows' lists took ~0.5 us of L2 latency per entry.)
+__device__ __noinline__ void outlier_chunk(const MmaParams& p, int m_first, int n, float* corr) {
+  constexpr int T = 8;
+  const int lane = int(threadIdx.x) & 31;
+  const int r = lane & 15, hi = lane >> 4;
+  const int2* lst = p.olist + int64_t(m_first + r) * kOutlierCap;
+  const uint2* wpair = reinterpret_cast<const uint2*>(p.wrows + ((n - lane) >> 4));  // (n - lane: a multiple of 32)
+  const int64_t kstride = p.N_pad >> 5;  // row pitch of the plane in word pairs
   const int sh = 2 * (n & 15);
-  float acc = 0.f;
+  const int cnt = __ldg(p.ocount + m_first + r);
+  float acc[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+  int maxcnt = kOutlierCap;  // (known after the first batch's loads are issued)
 #pragma unroll 1
-  for (int i0 = 0; i0 < cnt; i0 += 8) {
-    int2 e[8];
-    uint32_t w[8];
+  for (int i0 = 0; i0 < maxcnt; i0 += 2 * T) {
+    int2 e[T];
+    uint2 wv[T];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) e[t] = i0 + t < cnt ? __ldg(lst + i0 + t) : make_int2(0, 0);  // (k = 0, x = 0: adds 0)
+    for (int t = 0; t < T; ++t) {  // (speculative: slots beyond the count hold stale pairs, masked below)
+      const int i = i0 + 2 * t + hi;
+      e[t] = i < kOutlierCap ? __ldg(lst + i) : make_int2(0, 0);
+    }
+    if (i0 == 0) {
+      maxcnt = cnt;
+      for (int o = 8; o; o >>= 1) maxcnt = max(maxcnt, __shfl_xor_sync(0xffffffffu, maxcnt, o));
+    }
 #pragma unroll
-    for (int t = 0; t < 8; ++t) w[t] = __ldg(col + int64_t(e[t].x) * kstride);
+    for (int t = 0; t < T; ++t) {
+      const bool live = i0 + 2 * t + hi < cnt;
+      if (!live) e[t] = make_int2(0, 0);  // (x = 0, codes 0: adds 0)
+      wv[t] = live ? __ldg(wpair + int64_t(e[t].x) * kstride) : make_uint2(0u, 0u);
+    }
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const uint32_t code = (w[t] >> sh) & 3u;
-      const float x = __int_as_float(e[t].y);
-      acc += code == 1u ? x : (code == 3u ? -x : 0.f);
+    for (int t = 0; t < T; ++t) {
+      if (i0 + 2 * t >= maxcnt) break;  // (warp-uniform)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // entry i0 + 2t (held by lanes 0-15), then i0 + 2t + 1 (lanes 16-31)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int src = 16 * h + j;
+          const float x = __int_as_float(__shfl_sync(0xffffffffu, e[t].y, src));
+          const uint32_t w0 = __shfl_sync(0xffffffffu, wv[t].x, src), w1 = __shfl_sync(0xffffffffu, wv[t].y, src);
+          const uint32_t code = ((hi ? w1 : w0) >> sh) & 3u;
+          acc[j] += code == 1u ? x : (code == 3u ? -x : 0.f);
+        }
+      }
     }
   }
-  return acc;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) corr[j] = acc[j];
 }
 
 // from the three limb sums of a finished accumulator (TMEM)
@@ -1132,8 +1181,6 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
             w[c][1] = lds128(src + 16u);
           }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_empty[sp]);  // packed tile consumed (values are in registers)
         // slot a was last read by the MMAs of iteration it - AS, released with stage
         // (it - AS) % S (at most one phase behind: STAGES >= A_SLOTS)
         if (it >= uint32_t(AS)) {
@@ -1159,6 +1206,14 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
             tmem_st32(tmem_base + lane_addr + uint32_t(C::A_BASE + a * C::A_COLS + c * 32), v);
           }
         }
+        // The packed tile is released only here, after the tcgen05.st that consumed the decoded
+        // words: every lane's ld.shared has then delivered its data.  Released right after the
+        // loads were ISSUED (as it was), the arrive could overtake loads still in flight when the
+        // load/store pipe was busy (the epilogue's outlier lookups), the W producer refilled the
+        // slot, and single lanes decoded the next tile's bytes: wrong W^T rows for a stage,
+        // non-deterministically (8192 x 8192 x 1024 with outlier rows, profiles/r02_v3/README).
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_empty[sp]);
         tmem_st_wait();
         // the MMA waits only on a_full: make it imply that this stage's X limbs landed too
         mbar_wait(&full_raw[s], r & 1);
@@ -1217,14 +1272,11 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
       // limbs): summed here, while the unit's MMAs run, so the lookups hide behind them.
       float corr[16 * ((MT + 31) / 32)];
       auto fill_corr = [&]() {
-        if (!n_ok) return;
+        if (ghost) return;  // (warp-uniform; padded columns n < N_pad read valid words)
 #pragma unroll 1
         for (int mm = 16 * half; mm < MT; mm += 32) {
           const uint32_t bits = (omask[mm >> 5] >> (mm & 31)) & 0xFFFFu;
-          if (!bits) continue;
-#pragma unroll 1
-          for (int j = 0; j < 16; ++j)
-            corr[(mm >> 5) * 16 + j] = ((bits >> j) & 1u) ? outlier_sum(p, m0 + mm + j, n) : 0.f;
+          if (bits) outlier_chunk(p, m0 + mm, n, corr + (mm >> 5) * 16);  // (warp-uniform)
         }
       };
       if (p.splits == 1) fill_corr();

@@ -250,8 +250,10 @@ __device__ __forceinline__ typename S::V column_value(const GatherArgs& a, int64
   }
 }
 
-// Runtime dispatch of the one-row (SrcRow) evaluation, for the fix-up paths.
-__device__ __forceinline__ float column_value_row(int var, const GatherArgs& a, int64_t n, float b, const float* xrow,
+// Runtime dispatch of the one-row (SrcRow) evaluation, for the fix-up paths.  Out of line: the
+// eight inlined walks are ~38 K SASS lines, which otherwise sit in the middle of the tensor-core
+// kernel between its warp roles' hot loops (the fix-up is the rare, slow path anyway).
+static __device__ __noinline__ float column_value_row(int var, const GatherArgs& a, int64_t n, float b, const float* xrow,
                                                   int32_t K, bool banked) {
   const SrcRow src{xrow, K};
   const unsigned br = banked ? 1u : 0u;
