@@ -725,7 +725,7 @@ def run_ours(args) -> None:
     ops_loc = ops(M, w_loc, nnz_local)
     bytes_loc = algorithmic_bytes(M, K, w_loc, nnz_local)
     t_kernel = max(t_run if method == "mma" else t_prep + t_run, 1e-6)
-    kern_name = "tg_mma_kernel" if method == "mma" else "tg_gather_kernel"
+    kern_name = "tg_mma_kernel" if method == "mma" else "tg_gather_staged_kernel"
     t_add = ops_loc / (p_add * 1e12)
     t_hbm = bytes_loc / (NOMINAL_HBM_GBS * 1e9)
     bound = "hbm" if t_hbm > t_add else "fp32_add"

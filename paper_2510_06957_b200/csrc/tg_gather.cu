@@ -139,13 +139,14 @@ struct Window {
   int32_t k1;          // the column pauses at the first stream index >= k1 (INT32_MAX in a sweep's last window)
 };
 
-// bit c of P set: component c is subtracted
-template <int P>
-__device__ __forceinline__ void acc4(float4& acc, const float4 x0, const float4 x1, const float4 x2, const float4 x3) {
-  if (P & 1) sub_(acc, x0); else add_(acc, x0);
-  if (P & 2) sub_(acc, x1); else add_(acc, x1);
-  if (P & 4) sub_(acc, x2); else add_(acc, x2);
-  if (P & 8) sub_(acc, x3); else add_(acc, x3);
+// acc +- x as fma(x, +-1, acc): x * (+-1) is exact, so the single rounding is that of the
+// reference's add / subtract, bit for bit -- and the sign is data, not a branch (the switch over
+// the four sign phases of a group took 45% of the kernel's stall samples).
+__device__ __forceinline__ void fma4(float4& acc, const float4 x, const float m) {
+  acc.x = __fmaf_rn(x.x, m, acc.x);
+  acc.y = __fmaf_rn(x.y, m, acc.y);
+  acc.z = __fmaf_rn(x.z, m, acc.z);
+  acc.w = __fmaf_rn(x.w, m, acc.w);
 }
 
 // Sign of stream position t (relative to the segment start): GM 0 = one sign for the whole
@@ -186,15 +187,17 @@ __device__ __forceinline__ int32_t walk_staged(float4& acc, const int32_t* __res
         const float4 x0 = w.base[d0 * (G_ROWS / 4)], x1 = w.base[d1 * (G_ROWS / 4)];
         const float4 x2 = w.base[d2 * (G_ROWS / 4)], x3 = w.base[d3 * (G_ROWS / 4)];
         if (GM == 0) {
-          if (neg0) acc4<15>(acc, x0, x1, x2, x3);
-          else acc4<0>(acc, x0, x1, x2, x3);
-        } else {
-          switch ((pq - s0) & 3) {  // runs of two: + + - - from a position that is 0 mod 4
-            case 0: acc4<12>(acc, x0, x1, x2, x3); break;
-            case 1: acc4<6>(acc, x0, x1, x2, x3); break;
-            case 2: acc4<3>(acc, x0, x1, x2, x3); break;
-            default: acc4<9>(acc, x0, x1, x2, x3); break;
-          }
+          const float m = neg0 ? -1.f : 1.f;
+          fma4(acc, x0, m);
+          fma4(acc, x1, m);
+          fma4(acc, x2, m);
+          fma4(acc, x3, m);
+        } else {  // runs of two from the segment start: the sign of position t is bit 1 of t - s0
+          const uint32_t ph = uint32_t(pq - s0);
+          fma4(acc, x0, (ph & 2u) ? -1.f : 1.f);
+          fma4(acc, x1, ((ph + 1u) & 2u) ? -1.f : 1.f);
+          fma4(acc, x2, ((ph + 2u) & 2u) ? -1.f : 1.f);
+          fma4(acc, x3, ((ph + 3u) & 2u) ? -1.f : 1.f);
         }
         continue;
       }
@@ -205,8 +208,7 @@ __device__ __forceinline__ int32_t walk_staged(float4& acc, const int32_t* __res
         if (k >= w.k1) return pq + c;  // paused: the next window (or sweep end) resumes here
         const uint32_t d = uint32_t(k - w.k0);
         const float4 x = d < w.nk ? w.base[d * (G_ROWS / 4)] : glob(k);
-        if (is_neg<GM>(pq + c - s0, g, neg0)) sub_(acc, x);
-        else add_(acc, x);
+        fma4(acc, x, is_neg<GM>(pq + c - s0, g, neg0) ? -1.f : 1.f);
       }
     }
     i = jend;

@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(XS_THREADS) tg_xsplit_kernel(const float* __re
 // more cover the reductions and the outlier rounds): the split is a streaming kernel and
 // wants bytes in flight.
 constexpr int xs_min_blocks(int threads, int ept) {
-  if (threads >= 512) return 1;  // (the wide CTAs serve few-row inputs: occupancy is not their bound)
+  if (threads >= 512) return ept <= 16 ? 2 : 1;  // (two wide CTAs per SM, as the few-row launch plan assumes)
   const int b = 65536 / (threads * (48 + 2 * ept));
   return b < 1 ? 1 : (b > 4 ? 4 : b);
 }
@@ -622,7 +622,7 @@ __device__ __forceinline__ void peer_store(const MmaParams& p, int64_t off, floa
 
 // Tile configuration.  A pipeline stage covers 256 k (two 128-k chunks: 8
 // MMAs of K = 32 and ONE tcgen05.commit -- a commit costs about as much as an
-// MMA, so 4-MMA stages ran at ~55% of the issue rate, scratch/mma_bench.cu).
+// MMA, so 4-MMA stages ran at ~55% of the issue rate: a round-1 probe; csrc/tg_peak.cu is its kept form).
 // TMEM (512 columns x 128 lanes x 32 bit) holds ACC_BUFS accumulators of NMMA
 // int32 columns plus two 64-column slots of the decoded W^T tile (128 lanes x
 // 256 int8): the expanded ternary tile never touches shared memory, which
@@ -662,7 +662,11 @@ struct MmaCfg {
   static constexpr int SMEM =
       STAGES * B_BYTES + P_STAGES * P_BYTES + Y_BYTES + 1024 /*align*/ + 2048 /*barriers, scales*/;
   static constexpr int EPI_WARP0 = 7;            // warps: 0 X producer, 1 MMA, 2-5 decoders, 6 W producer
-  static constexpr int EPI_WARPS = 8;            // two per TMEM lane quarter, splitting the rows
+  // two per TMEM lane quarter, splitting the 16-row chunks; one per quarter at MT <= 32 (one or two
+  // chunks): 480 threads instead of 608 leave 128 registers per thread, and the small-tile
+  // kernel no longer spills (a spilled register costs a DRAM round trip after an L2 flush)
+  static constexpr int EPI_WARPS = MT <= 32 ? 4 : 8;
+  static constexpr int EPI_HALVES = EPI_WARPS / 4;
   // Small MT: N <= 96 MMAs take ~60 cycles each, faster than one decoder group expands a
   // stage (~700 cycles, mostly latency), so a second group (warps 15-18) takes every other
   // stage.
@@ -692,7 +696,7 @@ __device__ __forceinline__ void unit_coords(const MmaParams& p, int u, int crank
 //   y = fp32(S0 2^(16-s) + S1 2^(8-s) + S2 2^-s + b) with three FMAs on the exact
 //   float limb sums (|S_l| < 2^24), PReLU, and write y into the smem Y tile (or
 //   straight to Y).  No FP64 and no 64-bit conversions on this path (each costs
-//   ~13 issue cycles per warp on B200, scratch/cvt_bench.cu).  For integer-valued
+//   ~13 issue cycles per warp on B200, a round-1 probe).  For integer-valued
 //   X the low limbs are zero and every step is exact.  The per-row scales
 //   {2^-s, 2^(8-s), 2^(16-s), 2^(24-s)} are staged in shared memory; rows whose
 //   scale leaves the float range are "wide" and recomputed exactly afterwards
@@ -716,7 +720,7 @@ struct EmitCtx {
 };
 
 // Row scales of 16 consecutive rows.  Full form: {2^-s, 2^(8-s), 2^(16-s), 2^(24-s)} per row
-// (one ld.shared.v4 each).  Compact form (the 608-thread small-tile kernels, whose register
+// (one ld.shared.v4 each).  Compact form (the small-tile kernels, MT <= 32, whose register
 // budget is 104): 2^-s only; 2^(8-s) and 2^(16-s) are exact power-of-two multiples of it for
 // every row whose scale is in range (the others are "wide" and recomputed).  Measured: the
 // full form is ~4% faster at MT = 64, the compact one avoids spills at MT <= 32 (cfg4 -2 us).
@@ -870,59 +874,49 @@ __device__ __forceinline__ void host_copy_tile(const MmaParams& p, const float* 
 
 // Outlier terms of 16 consecutive rows for this lane's column n: corr[r] = sum over row
 // (m_first + r)'s listed entries of W[k, n] * x, in list order (ascending k: a fixed order).
-// The whole warp cooperates, in two memory round trips per batch of 16 entries of every row:
-//   1. lane l loads entries i0 + 2t + l / 16 (t < 8) of row l % 16, together with the row's count;
-//   2. lane l loads, for each of ITS entries, the two words of the row-major 2-bit plane behind
-//      the tiles that hold W[k, .] for the warp's 32 columns (16 columns per word) -- the 256
-//      (row, entry) pairs of the batch are all in flight at once;
-// then every pair's (x, word pair) is broadcast by shuffle and each lane adds its column's term.
-// (One lane per column walking its rows' lists took ~0.5 us of L2 latency per entry.)
+// The whole warp cooperates, in two memory round trips:
+//   1. lane l loads entry l of each of the 16 lists (a list is 32 slots = 256 contiguous bytes;
+//      slots beyond a row's count hold stale pairs and are masked), with the 16 counts;
+//   2. lane l loads, for each of ITS 16 entries, the two words of the row-major 2-bit plane
+//      behind the tiles that hold W[k, .] for the warp's 32 columns (16 columns per word);
+// then entry i of every row is broadcast from lane i by shuffle (a rolled loop over i, the rows
+// unrolled) and each lane adds its column's term.  Branch-free: bit 1 of a code flips the sign
+// of x, bit 0 selects x or 0.  (One lane per column walking its rows' lists paid ~0.5 us of L2
+// latency per entry; a fully unrolled (entry, row) nest was 150 KB of code, fetch-bound.)
 __device__ __noinline__ void outlier_chunk(const MmaParams& p, int m_first, int n, float* corr) {
-  constexpr int T = 8;
+  static_assert(kOutlierCap == 32, "one list slot per lane");
   const int lane = int(threadIdx.x) & 31;
-  const int r = lane & 15, hi = lane >> 4;
-  const int2* lst = p.olist + int64_t(m_first + r) * kOutlierCap;
+  const int hi = lane >> 4;
+  const int2* lst = p.olist + int64_t(m_first) * kOutlierCap + lane;
   const uint2* wpair = reinterpret_cast<const uint2*>(p.wrows + ((n - lane) >> 4));  // (n - lane: a multiple of 32)
   const int64_t kstride = p.N_pad >> 5;  // row pitch of the plane in word pairs
   const int sh = 2 * (n & 15);
-  const int cnt = __ldg(p.ocount + m_first + r);
+  const int cnt_l = __ldg(p.ocount + m_first + (lane & 15));  // lane j (and j + 16) holds row j's count
+  int2 e[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) e[j] = __ldg(lst + j * kOutlierCap);
+  int maxcnt = cnt_l;
+  for (int o = 8; o; o >>= 1) maxcnt = max(maxcnt, __shfl_xor_sync(0xffffffffu, maxcnt, o));
+  uint2 wv[16];
+  float xv[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const bool live = lane < __shfl_sync(0xffffffffu, cnt_l, j);
+    xv[j] = live ? __int_as_float(e[j].y) : 0.f;  // (x = 0, codes 0: adds 0)
+    wv[j] = live ? __ldg(wpair + int64_t(e[j].x) * kstride) : make_uint2(0u, 0u);
+  }
   float acc[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-  int maxcnt = kOutlierCap;  // (known after the first batch's loads are issued)
 #pragma unroll 1
-  for (int i0 = 0; i0 < maxcnt; i0 += 2 * T) {
-    int2 e[T];
-    uint2 wv[T];
+  for (int i = 0; i < maxcnt; ++i) {
 #pragma unroll
-    for (int t = 0; t < T; ++t) {  // (speculative: slots beyond the count hold stale pairs, masked below)
-      const int i = i0 + 2 * t + hi;
-      e[t] = i < kOutlierCap ? __ldg(lst + i) : make_int2(0, 0);
-    }
-    if (i0 == 0) {
-      maxcnt = cnt;
-      for (int o = 8; o; o >>= 1) maxcnt = max(maxcnt, __shfl_xor_sync(0xffffffffu, maxcnt, o));
-    }
-#pragma unroll
-    for (int t = 0; t < T; ++t) {
-      const bool live = i0 + 2 * t + hi < cnt;
-      if (!live) e[t] = make_int2(0, 0);  // (x = 0, codes 0: adds 0)
-      wv[t] = live ? __ldg(wpair + int64_t(e[t].x) * kstride) : make_uint2(0u, 0u);
-    }
-#pragma unroll
-    for (int t = 0; t < T; ++t) {
-      if (i0 + 2 * t >= maxcnt) break;  // (warp-uniform)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {  // entry i0 + 2t (held by lanes 0-15), then i0 + 2t + 1 (lanes 16-31)
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int src = 16 * h + j;
-          const float x = __int_as_float(__shfl_sync(0xffffffffu, e[t].y, src));
-          const uint32_t w0 = __shfl_sync(0xffffffffu, wv[t].x, src), w1 = __shfl_sync(0xffffffffu, wv[t].y, src);
-          const uint32_t code = ((hi ? w1 : w0) >> sh) & 3u;
-          acc[j] += code == 1u ? x : (code == 3u ? -x : 0.f);
-        }
-      }
+    for (int j = 0; j < 16; ++j) {
+      const float x = __shfl_sync(0xffffffffu, xv[j], i);
+      const uint32_t w0 = __shfl_sync(0xffffffffu, wv[j].x, i), w1 = __shfl_sync(0xffffffffu, wv[j].y, i);
+      const uint32_t code = (hi ? w1 : w0) >> sh;
+      const float xs = __int_as_float(__float_as_int(x) ^ int((code & 2u) << 30));
+      acc[j] += (code & 1u) ? xs : 0.f;
     }
   }
 #pragma unroll
@@ -1181,6 +1175,23 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
             w[c][1] = lds128(src + 16u);
           }
         }
+        // The packed tile goes back to the W producer as soon as its words are in registers --
+        // really in registers: the arrive's address carries a data dependence on one word of
+        // every ld.shared above (dep ^ own-lane shuffle of dep = 0), so the instruction cannot issue before
+        // the loads have delivered.  Released right after the loads were ISSUED (as it was in
+        // round 1), the arrive could overtake loads still in flight when the load/store pipe
+        // was busy (the epilogue's outlier lookups), the producer refilled the slot, and single
+        // lanes decoded the next tile's bytes: wrong W^T rows for a stage, non-deterministically
+        // (8192 x 8192 x 1024 with outlier rows, profiles/r02_v3/README.md).
+        {
+          uint32_t dep = w[0][0].x ^ w[0][1].x;
+          if (nch > 1) dep ^= w[1][0].x ^ w[1][1].x;
+          // (a constant-foldable `and dep, 0` does not survive ptxas; a lane's own value through
+          // the shuffle network does, and the shuffle queues behind the loads in the same pipe)
+          const uint32_t zero = __shfl_sync(0xffffffffu, dep, lane) ^ dep;
+          __syncwarp();
+          if (lane == 0) mbar_arrive(reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(&p_empty[sp]) + zero));
+        }
         // slot a was last read by the MMAs of iteration it - AS, released with stage
         // (it - AS) % S (at most one phase behind: STAGES >= A_SLOTS)
         if (it >= uint32_t(AS)) {
@@ -1206,14 +1217,6 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
             tmem_st32(tmem_base + lane_addr + uint32_t(C::A_BASE + a * C::A_COLS + c * 32), v);
           }
         }
-        // The packed tile is released only here, after the tcgen05.st that consumed the decoded
-        // words: every lane's ld.shared has then delivered its data.  Released right after the
-        // loads were ISSUED (as it was), the arrive could overtake loads still in flight when the
-        // load/store pipe was busy (the epilogue's outlier lookups), the W producer refilled the
-        // slot, and single lanes decoded the next tile's bytes: wrong W^T rows for a stage,
-        // non-deterministically (8192 x 8192 x 1024 with outlier rows, profiles/r02_v3/README).
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_empty[sp]);
         tmem_st_wait();
         // the MMA waits only on a_full: make it imply that this stage's X limbs landed too
         mbar_wait(&full_raw[s], r & 1);
@@ -1232,7 +1235,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
     const int et = threadIdx.x - 32 * C::EPI_WARP0;  // 0..ET-1
     const int half = (warp - C::EPI_WARP0) >> 2;
     const uint32_t rs_addr = smem_u32(rs_s);
-    constexpr bool COMPACT = C::DEC_GROUPS > 1;     // (the 608-thread kernels: see load_scales)
+    constexpr bool COMPACT = C::DEC_GROUPS > 1;     // (the small-tile kernels: see load_scales)
     float* sc_s = reinterpret_cast<float*>(rs_s);  // [80] row scales of the unit (x4 when !COMPACT)
     uint32_t* wmask = reinterpret_cast<uint32_t*>(rs_s + 160);  // [4] wide-row bits of the unit (after 80 float4)
     uint32_t* omask = reinterpret_cast<uint32_t*>(rs_s + 163);  // [4] rows with listed outliers (after the PReLU count)
@@ -1270,17 +1273,22 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
       named_bar_sync(1, ET);
       // Outlier terms of this thread's rows (the X split listed the entries it kept out of the
       // limbs): summed here, while the unit's MMAs run, so the lookups hide behind them.
-      float corr[16 * ((MT + 31) / 32)];
+      constexpr int MSTEP = 16 * C::EPI_HALVES;  // rows between two chunks of one warp
+      constexpr int MSHIFT = C::EPI_HALVES == 2 ? 5 : 4;
+      float corr[16 * ((MT + MSTEP - 1) / MSTEP)];
       auto fill_corr = [&]() {
         if (ghost) return;  // (warp-uniform; padded columns n < N_pad read valid words)
 #pragma unroll 1
-        for (int mm = 16 * half; mm < MT; mm += 32) {
+        for (int mm = 16 * half; mm < MT; mm += MSTEP) {
           const uint32_t bits = (omask[mm >> 5] >> (mm & 31)) & 0xFFFFu;
-          if (bits) outlier_chunk(p, m0 + mm, n, corr + (mm >> 5) * 16);  // (warp-uniform)
+          if (bits) outlier_chunk(p, m0 + mm, n, corr + (mm >> MSHIFT) * 16);  // (warp-uniform)
         }
       };
+      if (et == 0 && lu == 0) TG_GT(8);
       if (p.splits == 1) fill_corr();
+      if (et == 0 && lu == 0) TG_GT(9);
       mbar_wait(&tfull[acc], use & 1);
+      if (et == 0 && lu == 0) TG_GT(10);
       if (et == 0) TG_STAMP(7, 2 + 2 * lu);
       tc_fence_after();
       const uint32_t tbase = tmem_base + acc * C::ACC_COLS + (uint32_t(q * 32) << 16);
@@ -1291,7 +1299,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
         e.bf = bf;
         e.wide_bits = (wmask[mm >> 5] >> (mm & 31)) & 0xFFFFu;
         e.out_bits = (omask[mm >> 5] >> (mm & 31)) & 0xFFFFu;
-        e.corr = corr + (mm >> 5) * 16;
+        e.corr = corr + (mm >> MSHIFT) * 16;
         e.m_first = m0 + mm;
         e.nlive = min(16, p.M - (m0 + mm));
         e.nvalid = e.nlive;
@@ -1306,7 +1314,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
         return e;
       };
 #pragma unroll 1
-      for (int mm = 16 * half; mm < MT; mm += 32) {
+      for (int mm = 16 * half; mm < MT; mm += MSTEP) {
         if (et == 0 && lu == 0) TG_STAMP(7, 200 + mm / 16);
         uint32_t r0[16], r1[16], r2[16];
 #ifdef TG_EPI_NOLDTM
@@ -1357,7 +1365,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
           __threadfence();
           fill_corr();
 #pragma unroll 1
-          for (int j0 = 16 * half; j0 < MT; j0 += 32) {
+          for (int j0 = 16 * half; j0 < MT; j0 += MSTEP) {
             // 16 independent rows per batch so the L2 reads of the partials overlap;
             // int32 sums stay exact (|S_l| < 128 K < 2^31)
             const int64_t plane = int64_t(p.M_pad) * p.N_pad;
@@ -1394,7 +1402,7 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
             const int j = 32 * w + (__ffs(bits) - 1);
             bits &= bits - 1;
             const int m = m0 + j;
-            if (m >= p.M || ((j >> 4) & 1) != half) continue;
+            if (m >= p.M || ((j >> 4) & (C::EPI_HALVES - 1)) != half) continue;
             float y = column_value_row(p.fix_var, p.fix, n, bf, p.X + int64_t(m) * p.ldx, p.K, m < p.m_full);
             if (p.use_alpha && !(y > 0.f)) {
               y = p.alpha * y;
@@ -1665,7 +1673,7 @@ int mma_pick_mt(int64_t M) {
   if (M <= 16) return 16;
   if (M <= 32) return 32;
   if (M <= 48) return 48;
-  // MT = 80 (MMA N = 240) hides the per-stage commit inside the longer MMAs (scratch/mma_bench.cu:
+  // MT = 80 (MMA N = 240) hides the per-stage commit inside the longer MMAs (round-1 probe:
   // 131 cycles per 128x240x32 MMA with a commit every 8, at the issue-rate peak) but has room for
   // one TMEM accumulator only, so its epilogue is not overlapped: worth it for tall X (many units
   // per CTA) whose padding to 80 rows is small.

@@ -11,7 +11,8 @@ Per milestone it prints min / max over the CTAs in microseconds from the first s
 start, the median over `reps` graph replays, each after a 256 MB L2 flush.  Milestones
 (TG_GT in csrc/tg_mma.cu): 0 split CTA start, 1 split row done, 2 GEMM CTA start, 3
 griddepcontrol.wait returned, 4 first MMA stage committed, 5 last MMA issued, 6 epilogue
-done, 7 CTA exit.  Not a bench number: the stamps cost a few hundred ns.
+done, 7 CTA exit, 8-10 (first unit of each CTA) the epilogue's outlier-term lookups and the
+moment its accumulator is ready.  Not a bench number: the stamps cost a few hundred ns.
 """
 from __future__ import annotations
 
@@ -28,7 +29,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 NAMES = ["split CTA start", "split row done", "GEMM CTA start", "dep wait returned", "first MMA commit",
-         "last MMA issued", "epilogue done", "CTA exit"]
+         "last MMA issued", "epilogue done", "CTA exit", "outlier terms: start", "outlier terms: done",
+         "accumulator ready"]
 
 
 def main() -> None:
@@ -67,7 +69,7 @@ def main() -> None:
         g.replay()
         torch.cuda.synchronize()
         lib.tg_debug_gt(out, 0)
-        v = np.array(out[:], dtype=np.uint64).reshape(16, 2)[:8].astype(np.int64)
+        v = np.array(out[:], dtype=np.uint64).reshape(16, 2)[:len(NAMES)].astype(np.int64)
         rows.append((v - v[0, 0]) / 1e3)
     rows = np.array(rows[3:])
     print(f"{args.config} x_outliers={args.x_outliers}: median over {args.reps} replays, us from the first split CTA")

@@ -112,3 +112,27 @@ def test_staged_gather_full_cfg2_slice(tg):
     y = tg.gemm_vectorized_optimal(tg.pad_input(torch.from_numpy(X).cuda()), fmt, b, 0.25, method="gather").values
     ref = orc.gemm_vectorized_optimal(orc.pad_input(X), orc.interleaved_blocked_from_dense(W, None, 2, True), b, 0.25)
     assert np.array_equal(y, ref)
+
+
+@pytest.mark.parametrize("p_pos,p_neg", [(0.45, 0.05), (0.05, 0.45), (0.3, 0.2)])
+def test_staged_gather_sign_imbalance_drift(tg, p_pos, p_neg):
+    """Unequal +1 / -1 densities: the two subsequences of the interleaved segment drift apart
+    linearly in k, so most operands of the slower one lie outside the staged window and take
+    the L2 path; long remainder segments follow.  Still bit-identical."""
+    from oracle import oracle as orc
+
+    rng = np.random.default_rng(int(p_pos * 100) * 7 + 3)
+    M, K, N = 200, 3000, 124
+    u = rng.random((K, N))
+    W = np.where(u < p_pos, 1, np.where(u < p_pos + p_neg, -1, 0)).astype(np.int8)
+    X = rng.standard_normal((M, K)).astype(np.float32)
+    b = rng.standard_normal(N).astype(np.float32)
+    Wd, Xd = tg.TernaryDense(torch.from_numpy(W).cuda()), torch.from_numpy(X).cuda()
+    for B in (None, 1024, 700):
+        ibs, ris = tg.interleaved_blocked_from_dense(Wd, B, 2, True), orc.interleaved_blocked_from_dense(W, B, 2, True)
+        ys, yp = _both_modes(lambda: tg.gemm_vectorized_optimal(tg.pad_input(Xd), ibs, b, 0.25, method="gather").values)
+        ref = orc.gemm_vectorized_optimal(orc.pad_input(X), ris, b, 0.25)
+        assert np.array_equal(ys, ref) and np.array_equal(yp, ref), B
+        ib, ri = tg.interleaved_blocked_from_dense(Wd, B, 2), orc.interleaved_blocked_from_dense(W, B, 2)
+        ys = tg.gemm_interleaved_blocked(Xd, ib, b, method="gather").values
+        assert np.array_equal(ys, orc.gemm_interleaved_blocked(X, ri, b)), B
