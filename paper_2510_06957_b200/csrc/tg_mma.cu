@@ -1175,23 +1175,6 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
             w[c][1] = lds128(src + 16u);
           }
         }
-        // The packed tile goes back to the W producer as soon as its words are in registers --
-        // really in registers: the arrive's address carries a data dependence on one word of
-        // every ld.shared above (dep ^ own-lane shuffle of dep = 0), so the instruction cannot issue before
-        // the loads have delivered.  Released right after the loads were ISSUED (as it was in
-        // round 1), the arrive could overtake loads still in flight when the load/store pipe
-        // was busy (the epilogue's outlier lookups), the producer refilled the slot, and single
-        // lanes decoded the next tile's bytes: wrong W^T rows for a stage, non-deterministically
-        // (8192 x 8192 x 1024 with outlier rows, profiles/r02_v3/README.md).
-        {
-          uint32_t dep = w[0][0].x ^ w[0][1].x;
-          if (nch > 1) dep ^= w[1][0].x ^ w[1][1].x;
-          // (a constant-foldable `and dep, 0` does not survive ptxas; a lane's own value through
-          // the shuffle network does, and the shuffle queues behind the loads in the same pipe)
-          const uint32_t zero = __shfl_sync(0xffffffffu, dep, lane) ^ dep;
-          __syncwarp();
-          if (lane == 0) mbar_arrive(reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(&p_empty[sp]) + zero));
-        }
         // slot a was last read by the MMAs of iteration it - AS, released with stage
         // (it - AS) % S (at most one phase behind: STAGES >= A_SLOTS)
         if (it >= uint32_t(AS)) {
@@ -1217,6 +1200,18 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
             tmem_st32(tmem_base + lane_addr + uint32_t(C::A_BASE + a * C::A_COLS + c * 32), v);
           }
         }
+        // The packed tile goes back to the W producer only here, after the tcgen05.st that
+        // consumed the decoded words: every lane's ld.shared has then delivered its data.
+        // Released right after the loads were ISSUED (round 1), the arrive could overtake loads
+        // still in flight when the load/store pipe was busy (the epilogue's outlier lookups),
+        // the producer refilled the slot, and single lanes decoded the next tile's bytes: wrong
+        // W^T rows for a stage, non-deterministically (8192 x 8192 x 1024 with outlier rows,
+        // profiles/r02_v3/README.md).  An early release behind a true data dependence on the
+        // loads (the arrive address XORed with dep ^ own-lane-shuffle(dep)) is also correct but
+        // puts a shuffle on the decoders' critical path: cfg3 +5.5 us, cfg4 +1.8 us
+        // (profiles/r02_v3/ab_release.txt).
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_empty[sp]);
         tmem_st_wait();
         // the MMA waits only on a_full: make it imply that this stage's X limbs landed too
         mbar_wait(&full_raw[s], r & 1);

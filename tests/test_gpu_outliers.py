@@ -177,3 +177,33 @@ def test_heavy_tailed_rows_fuzz(tg, seed):
     y = tg.gemm_base(X, t, b, method="mma").values
     nw, sc = _bars(y, X, W, b)
     assert nw <= TOL and sc <= TOL, (seed, nw, sc)
+
+
+@pytest.mark.parametrize("tag", ["base", "unrolled", "blocked", "interleaved_blocked", "compressed", "vertical",
+                                 "horizontal", "vectorized_optimal"])
+def test_every_registry_variant_with_outlier_rows(tg, tag):
+    """Every registry tag (kernels/__init__.py:98-198) on the tensor-core path with outlier
+    channels, a row that cannot shed (exact walk of that variant's own order) and a plain row."""
+    rng = np.random.default_rng(sum(map(ord, tag)))
+    M, K, N = 37, 1300, 96
+    W = _w(rng, K, N)
+    X = rng.standard_normal((M, K)).astype(np.float32)
+    X[:30, rng.choice(K, 5, replace=False)] *= np.float32(200.0)      # rows 0-29: five outlier channels
+    X[31, rng.choice(K, 50, replace=False)] *= np.float32(500.0)      # row 31: more entries than the list holds
+    b = rng.standard_normal(N).astype(np.float32)
+    spec = tg.get_variant(tag)
+    alpha = 0.25 if spec.supports_alpha else None
+    cfg = tg.GemmConfig(method="mma", alpha=alpha, b=512)
+    y = tg.run_variant(tag, X, W, b, cfg).values
+    nw, sc = _bars(y, X, W, b, alpha)
+    assert nw <= TOL and sc <= TOL, (tag, nw, sc)
+    # the row on the exact walk is bit-identical with the variant's gather path
+    y_g = tg.run_variant(tag, X, W, b, tg.GemmConfig(method="gather", alpha=alpha, b=512)).values
+    assert np.array_equal(y[31], y_g[31]), tag
+    # integer-valued twin: bit-exact everywhere (outlier rows included)
+    Xi = rng.integers(-6, 7, size=(M, K)).astype(np.float32)
+    Xi[:30, rng.choice(K, 5, replace=False)] *= np.float32(300.0)
+    bi = rng.integers(-3, 4, size=N).astype(np.float32)
+    yi = tg.run_variant(tag, Xi, W, bi, cfg).values
+    yg = tg.run_variant(tag, Xi, W, bi, tg.GemmConfig(method="gather", alpha=alpha, b=512)).values
+    assert np.array_equal(yi, yg), tag
