@@ -201,15 +201,25 @@ __device__ __forceinline__ int32_t walk_staged(float4& acc, const int32_t* __res
         }
         continue;
       }
+      // Mixed group (a window edge, a segment end, an operand outside the window): no branch
+      // per component.  The first live component at or beyond k1 stops the group (the column
+      // pauses there); every component before it loads through ONE generic pointer -- the
+      // staged element or the transposed copy in L2 -- and its four FFMAs are predicated.
+      int cstop = c1 < 4 ? c1 : 4;
+#pragma unroll
+      for (int c = 3; c >= 0; --c)
+        if (c >= c0 && c < c1 && kk[c] >= w.k1) cstop = c;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        if (c < c0 || c >= c1) continue;
-        const int32_t k = kk[c];
-        if (k >= w.k1) return pq + c;  // paused: the next window (or sweep end) resumes here
+        const bool live = c >= c0 && c < cstop;
+        const int32_t k = live ? kk[c] : w.k0;  // (dead components read a valid staged element)
         const uint32_t d = uint32_t(k - w.k0);
-        const float4 x = d < w.nk ? w.base[d * (G_ROWS / 4)] : glob(k);
-        fma4(acc, x, is_neg<GM>(pq + c - s0, g, neg0) ? -1.f : 1.f);
+        const float4* src = d < w.nk ? w.base + d * (G_ROWS / 4)
+                                     : reinterpret_cast<const float4*>(glob.xt + int64_t(k) * glob.ld);
+        const float4 x = *src;
+        if (live) fma4(acc, x, is_neg<GM>(pq + c - s0, g, neg0) ? -1.f : 1.f);
       }
+      if (cstop < c1 && cstop < 4) return pq + cstop;  // paused: the next window (or sweep end) resumes here
     }
     i = jend;
   }
