@@ -330,6 +330,7 @@ namespace {
 // 1/P.streams of the SMs: a chunk's GEMM costs about as long as the whole
 // one (its fill, epilogue and W stream do not shrink with the rows), so run
 // one after another they would serialise the pipeline.
+constexpr int kMaxHostChunks = 16;  // (chunk events per device)
 struct HostPlan {
   int64_t rows, n;  // chunk height (the last one may be shorter), chunk count
   int streams;      // side streams used
@@ -362,8 +363,10 @@ bool host_zero_copy_x(const float* X_host, int64_t M, int64_t K) {
 HostPlan host_plan(int64_t M, int64_t K, int64_t N, bool x_in_place) {
   HostPlan P;
   const int64_t bytes = M * K * 4;
-  int64_t cap = 8;
-  if (const char* env = getenv("TG_HOST_CHUNKS")) cap = std::min(8, std::max(1, atoi(env)));  // (8 chunk events)
+  // (cfg5, 268 MB of X and 537 MB of Y: 8 chunks 11.77 ms, 12 chunks 11.44 ms, 16 chunks 11.54 ms --
+  // more chunks start the Y stream earlier, fewer keep the per-chunk GEMMs efficient)
+  int64_t cap = bytes >= (int64_t(128) << 20) ? 12 : 8;
+  if (const char* env = getenv("TG_HOST_CHUNKS")) cap = std::min(kMaxHostChunks, std::max(1, atoi(env)));
   // ~1 MB chunks for X read in place (<= 4 MB; cfg2: 4 chunks 0.243 ms, 1 chunk 0.25-0.26 ms),
   // ~2 MB for copied X (cfg3, 16 MB: 4 and 8 chunks within noise, 0.59-0.69 ms; cfg5: 8 chunks
   // 11.7 ms, 4 chunks 12.5 ms)
@@ -384,7 +387,7 @@ struct SideStreams {
   cudaStream_t s[4];       // chunk GEMMs (chunk c on s[c % 4])
   cudaStream_t cin, cout;  // the X chunks in, the Y chunks out, each in chunk order
   cudaEvent_t join[4];
-  cudaEvent_t xin[8], ydone[8];  // chunk c: X landed / Y computed
+  cudaEvent_t xin[kMaxHostChunks], ydone[kMaxHostChunks];  // chunk c: X landed / Y computed
   cudaEvent_t fork, join_in, join_out;
   cudaStream_t capture;
 };
@@ -404,7 +407,7 @@ int side_streams(SideStreams** out) {
           (e = cudaEventCreateWithFlags(&ss.join[i], cudaEventDisableTiming)) != cudaSuccess)
         return set_cuda_error(e, "side stream creation");
     }
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < kMaxHostChunks; ++i)
       if ((e = cudaEventCreateWithFlags(&ss.xin[i], cudaEventDisableTiming)) != cudaSuccess ||
           (e = cudaEventCreateWithFlags(&ss.ydone[i], cudaEventDisableTiming)) != cudaSuccess)
         return set_cuda_error(e, "side stream creation");

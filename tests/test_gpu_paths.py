@@ -290,3 +290,22 @@ def test_host_streaming_c_abi_pitched(tg, zerocopy_pitch, xmode, monkeypatch):
         assert torch.equal(yd[:, :N].cpu(), torch.from_numpy(ref))
         assert bool((xd[:, K:] == 0).all())
         assert int(fh[0]) == 0 and int(fh[1]) == 0
+
+
+def test_host_streaming_more_than_eight_chunks(tg, monkeypatch):
+    """26 MB of X with TG_HOST_CHUNKS=16: 12 row chunks (the plan very large X takes by
+    default, tg_capi.cu host_plan) through the 4 side streams and 16 chunk events; the result
+    equals the device-resident call bit for bit, replayed from the library's graph too."""
+    monkeypatch.setenv("TG_HOST_CHUNKS", "16")
+    rng = np.random.default_rng(33)
+    M, K, N = 3200, 2048, 256
+    W = rng.integers(-1, 2, size=(K, N)).astype(np.int8)
+    X = rng.standard_normal((M, K)).astype(np.float32)
+    X[::257, 11] = 4e4  # a few rows shed an outlier entry
+    b = rng.standard_normal(N).astype(np.float32)
+    ib = tg.interleaved_blocked_from_dense(torch.from_numpy(W).cuda())
+    ref = tg.gemm_interleaved_blocked(tg.DenseMatrix(torch.from_numpy(X).cuda()), ib, b, method="mma").values.copy()
+    Xpin = torch.from_numpy(X).pin_memory()
+    for _ in range(3):  # direct, captured, replayed
+        y = tg.gemm_interleaved_blocked(Xpin, ib, b, method="mma").values
+        assert np.array_equal(y, ref)
