@@ -189,3 +189,27 @@ def test_compute_entry_points_fail_loudly_without_gpu():
         pytest.skip("a GPU is present")
     with pytest.raises(RuntimeError):
         tg.tcsc_from_dense(np.zeros((2, 2), np.int8))
+
+
+def test_bench_arms_describe_the_same_workload():
+    """Both bench arms print config_dict(...) (the driver compares the two lines' `config`), the
+    default workload is the largest BASELINE config, and --x-outliers scales the same seeded
+    channels in either arm."""
+    import bench
+
+    assert bench.DEFAULT_CONFIG == "cfg5"
+    a, b = bench.config_dict("cfg5", 123), bench.config_dict("cfg5", 123)
+    assert a == b and a["workload"] == "cfg5" and (a["M"], a["K"], a["N"]) == (8192, 8192, 16384)
+    assert "x_outliers" not in a
+    o = bench.config_dict("cfg4", 7, "8@100")
+    assert o["x_outliers"].startswith("8@100") and o["workload"] == "cfg4"
+    assert bench.parse_outliers(None) is None and bench.parse_outliers("8@100") == (8, 100.0)
+    W0, X0, b0 = bench.bench_inputs("cfg1")
+    W1, X1, b1 = bench.bench_inputs("cfg1", "3@50")
+    W2, X2, b2 = bench.bench_inputs("cfg1", "3@50")
+    assert np.array_equal(W0, W1) and np.array_equal(b0, b1) and np.array_equal(X1, X2)
+    ch = np.flatnonzero((X1 != X0).any(axis=0))
+    assert len(ch) == 3 and np.array_equal(X1[:, ch], X0[:, ch] * np.float32(50.0))
+    # the integer-valued twin (dense.py:143-160) is never scaled: it must stay exact
+    _, Xi, _ = bench.bench_inputs("cfg1", "3@50", integer=True)
+    assert np.array_equal(Xi, bench.make_inputs("cfg1", integer=True)[1])
