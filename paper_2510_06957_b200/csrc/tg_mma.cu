@@ -315,6 +315,7 @@ __global__ void __launch_bounds__(THREADS, xs_min_blocks(THREADS, EPT)) tg_xspli
   __shared__ int red_i[NW];
   __shared__ int red_j[NW];
   __shared__ float red_g[NW];
+  __shared__ int red_k[NW];
   grid_dep_launch();  // the MMA kernel may start its prologue (it waits before reading our output)
   zero_split_counters(rscale, M_pad);
   if (threadIdx.x == 0) TG_GT(0);
@@ -334,14 +335,16 @@ __global__ void __launch_bounds__(THREADS, xs_min_blocks(THREADS, EPT)) tg_xspli
     for (int j = 0; j < EPT; ++j) x[j] = (in && k0 + j < K) ? __ldg(grow + k0 + j) : 0.f;
   }
   const int w = threadIdx.x >> 5;
-  // block-wide (max, sum, sum, sum, sum) of (float, float, double, int, int); every thread gets the result
-  auto reduce5 = [&](float& a, float& g, double& d, int& i, int& j2) {
+  // block-wide (max, sum, sum, sum, sum, sum) of (float, float, double, int, int, int); every thread
+  // gets the result; red_j keeps the per-warp partials of j2 until the next call
+  auto reduce6 = [&](float& a, float& g, double& d, int& i, int& j2, int& k3) {
     for (int o = 16; o; o >>= 1) {
       a = fmax_nan(a, __shfl_xor_sync(0xffffffffu, a, o));
       g += __shfl_xor_sync(0xffffffffu, g, o);
       d += __shfl_xor_sync(0xffffffffu, d, o);
       i += __shfl_xor_sync(0xffffffffu, i, o);
       j2 += __shfl_xor_sync(0xffffffffu, j2, o);
+      k3 += __shfl_xor_sync(0xffffffffu, k3, o);
     }
     __syncthreads();  // (the previous round's readers are done with the arrays)
     if ((threadIdx.x & 31) == 0) {
@@ -350,6 +353,7 @@ __global__ void __launch_bounds__(THREADS, xs_min_blocks(THREADS, EPT)) tg_xspli
       red_d[w] = d;
       red_i[w] = i;
       red_j[w] = j2;
+      red_k[w] = k3;
     }
     __syncthreads();
     a = red_f[0];
@@ -357,6 +361,7 @@ __global__ void __launch_bounds__(THREADS, xs_min_blocks(THREADS, EPT)) tg_xspli
     d = red_d[0];
     i = red_i[0];
     j2 = red_j[0];
+    k3 = red_k[0];
 #pragma unroll
     for (int q = 1; q < NW; ++q) {
       a = fmax_nan(a, red_f[q]);
@@ -364,6 +369,7 @@ __global__ void __launch_bounds__(THREADS, xs_min_blocks(THREADS, EPT)) tg_xspli
       d += red_d[q];
       i += red_i[q];
       j2 += red_j[q];
+      k3 += red_k[q];
     }
   };
   float amax = 0.f, s1 = 0.f;  // (s1 = sum |x| may overflow to inf for huge rows: the cut then falls back to the rms)
@@ -443,7 +449,8 @@ __global__ void __launch_bounds__(THREADS, xs_min_blocks(THREADS, EPT)) tg_xspli
       const float cut = kOutlierCut * fminf(float(sqrt(s2_r / double(nz_r))), 1.25f * s1_r / float(nz_r));
       float am = 0.f, ssf = 0.f, s1f = 0.f;  // (a thread's <= 32 terms in fp32, scaled by the cut: no overflow)
       const float icut = 1.f / cut;
-      int cnt = 0;
+      int cnt = 0, near = 0;  // near: nonzeros of the rest within kWideRatio of the CUT (a lower bound of
+                              // the second rule's count, which is relative to the rest's amax <= cut)
 #pragma unroll
       for (int j = 0; j < EPT; ++j) {
         const float a = fabsf(x[j]);
@@ -455,11 +462,12 @@ __global__ void __launch_bounds__(THREADS, xs_min_blocks(THREADS, EPT)) tg_xspli
           ssf = fmaf(t, t, ssf);
           s1f += t;
           cnt += a != 0.f;
+          near += t * kWideRatio >= 1.f;
         }
       }
       double ss = double(ssf) * double(cut) * double(cut);
       int no = __popc(omask);
-      reduce5(am, s1f, ss, cnt, no);
+      reduce6(am, s1f, ss, cnt, no, near);
       amax_r = am;
       s1_r = s1f * cut;
       s2_r = ss;
@@ -467,6 +475,10 @@ __global__ void __launch_bounds__(THREADS, xs_min_blocks(THREADS, EPT)) tg_xspli
       n_out = no;
       if (n_out > kOutlierCap || nz_r == 0) break;
       if (double(nz_r) * double(amax_r) * double(amax_r) > wide2 * s2_r) continue;  // still wide: next round
+      if (near * kWideFrac >= nz_r) {  // the second rule holds already by the lower bound
+        ok = true;
+        break;
+      }
       int big_r = 0;
 #pragma unroll
       for (int j = 0; j < EPT; ++j)
@@ -478,18 +490,16 @@ __global__ void __launch_bounds__(THREADS, xs_min_blocks(THREADS, EPT)) tg_xspli
       }
     }
     if (ok) {
-      // list the outliers in ascending k: exclusive prefix of the per-thread counts
+      // list the outliers in ascending k: exclusive prefix of the per-thread counts (the
+      // per-warp totals are the partials the last reduce6 left in red_j)
       const int mine = __popc(omask);
       int incl = mine;
       for (int o = 1; o < 32; o <<= 1) {
         const int t = __shfl_up_sync(0xffffffffu, incl, o);
         if ((threadIdx.x & 31) >= o) incl += t;
       }
-      __syncthreads();
-      if ((threadIdx.x & 31) == 31) red_i[w] = incl;
-      __syncthreads();
       int pos = incl - mine;
-      for (int q = 0; q < w; ++q) pos += red_i[q];
+      for (int q = 0; q < w; ++q) pos += red_j[q];
       int2* lst = outlier_list(rscale, M_pad) + m * kOutlierCap;
 #pragma unroll
       for (int j = 0; j < EPT; ++j) {
