@@ -295,12 +295,13 @@ __global__ void __launch_bounds__(XS_THREADS) tg_xsplit_kernel(const float* __re
 // converted from registers.  Digits: with |v| < 2^22, u = v + 0x808080 lies in
 // [0, 2^24) and byte i of u, minus 128, is the i-th balanced base-256 digit of v
 // (the same digits as limb_digits); as int8 that is byte ^ 0x80.
-// CTAs per SM the register allocation must allow (the row lives in EPT registers; about 48
-// more cover the reductions and the outlier rounds): the split is a streaming kernel and
-// wants bytes in flight.
+// CTAs per SM the register allocation must allow (the row lives in EPT registers): the split
+// is a streaming kernel and wants bytes in flight.  Three 256-thread CTAs of the 32-per-thread
+// variant per SM (80 registers, 4 bytes of spills) instead of two (98): cfg5's split 0.139 ->
+// 0.120 ms.
 constexpr int xs_min_blocks(int threads, int ept) {
   if (threads >= 512) return ept <= 16 ? 2 : 1;  // (two wide CTAs per SM, as the few-row launch plan assumes)
-  const int b = 65536 / (threads * (48 + 2 * ept));
+  const int b = 65536 / (threads * (20 + 2 * ept));
   return b < 1 ? 1 : (b > 4 ? 4 : b);
 }
 template <int THREADS, int EPT>
