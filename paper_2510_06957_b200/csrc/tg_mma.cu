@@ -109,9 +109,10 @@ __device__ __forceinline__ void zero_split_counters(double* rscale, int64_t M_pa
 // the rest).  A row whose amax is more than kWideRatio x the rms of its nonzeros would leave
 // the bulk of its entries only a few bits on the 22-bit grid.  Instead of sending the whole
 // row down the exact-order walk, the X split takes the few large entries out of the limbs:
-// entries beyond kOutlierCut x rms(the rest) are listed as (k, x) pairs (at most kOutlierCap
-// per row, in ascending k), the limbs carry the rest at the rest's own scale, and the GEMM
-// epilogue adds sum_k (+-x) of the listed entries from the packed tile words (exact fp32
+// entries beyond kOutlierCut x the scale of the rest (its rms, or 1.25 x its mean |x| when
+// that is smaller) are listed as (k, x) pairs (at most kOutlierCap per row, in ascending k),
+// the limbs carry the rest at the rest's own scale, and the GEMM epilogue adds sum_k (+-x) of
+// the listed entries, W[k, n] read from the row-major 2-bit plane behind the tiles (exact fp32
 // adds, a fixed order).  Rows that stay wide after kOutlierRounds rounds keep the exact walk.
 constexpr int kOutlierCap = 32;
 constexpr float kOutlierCut = 8.f;
