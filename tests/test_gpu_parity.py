@@ -367,6 +367,37 @@ def test_cfg5_rows_are_independent_and_match_oracle(tg):
     assert device_agreement(yi, dXi, dW, dbi, None)["exact"]
 
 
+def test_cfg5_size_independent_properties(tg):
+    """Properties that need no oracle, at cfg5's full size:
+    * linearity on integer-valued X (the reference's regime, dense.py:17-19): every step is
+      exact, so with b = 0, Y(X1 + X2) == Y(X1) + Y(X2) bit for bit;
+    * the gather path (reference order) equals the tensor-core path on an integer row slice;
+    * the format round trip: tiles -> dense W equals the W the format was built from, and the
+      device builder's index arrays are a permutation-free encoding (nnz preserved);
+    * negating W negates Y exactly (b = 0)."""
+    from paper_2510_06957_b200.workloads import make_inputs
+
+    W, _, b = make_inputs("cfg5")
+    M, K, N = 8192, 8192, 16384
+    dW = torch.from_numpy(W).cuda()
+    t = tg.interleaved_blocked_from_dense(tg.TernaryDense(dW), None, 2)
+    assert torch.equal(t.to_dense().device_values, dW)
+    g = torch.Generator(device="cuda").manual_seed(55)
+    X1 = torch.randint(-4, 5, (M, K), device="cuda", generator=g).float()
+    X2 = torch.randint(-4, 5, (M, K), device="cuda", generator=g).float()
+    zero = np.zeros(N, np.float32)  # (a real-valued b would round Y; the products themselves are exact)
+    z1 = tg.gemm_interleaved_blocked(X1, t, zero, method="mma").device_values
+    z2 = tg.gemm_interleaved_blocked(X2, t, zero, method="mma").device_values
+    z12 = tg.gemm_interleaved_blocked(X1 + X2, t, zero, method="mma").device_values
+    assert torch.equal(z12, z1 + z2)
+    rows = torch.arange(0, M, 64, device="cuda")
+    zg = tg.gemm_interleaved_blocked(X1[rows], t, zero, method="gather").device_values
+    assert torch.equal(zg, z1[rows])
+    tn = tg.interleaved_blocked_from_dense(tg.TernaryDense(-dW), None, 2)
+    zn = tg.gemm_interleaved_blocked(X1, tn, zero, method="mma").device_values
+    assert torch.equal(zn, -z1)
+
+
 # ---------------------------------------------------------------- edge cases
 
 
