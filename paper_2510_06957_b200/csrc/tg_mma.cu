@@ -492,6 +492,15 @@ __global__ void __launch_bounds__(THREADS, xs_min_blocks(THREADS, EPT)) tg_xspli
       }
     }
     if (ok) {
+      // the rest's scale must stay inside the epilogue's range: else the row keeps all its
+      // entries in the limbs and takes the exact walk (or, without an exact-order format, the
+      // fp64 recombination of the limb sums, which knows nothing of listed entries)
+      int e_r;
+      frexpf(amax_r, &e_r);
+      const int s_r = 22 - e_r;
+      ok = s_r <= kMaxScaleExp && s_r >= -kMaxScaleExp;
+    }
+    if (ok) {
       // list the outliers in ascending k: exclusive prefix of the per-thread counts (the
       // per-warp totals are the partials the last reduce6 left in red_j)
       const int mine = __popc(omask);

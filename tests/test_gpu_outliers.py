@@ -207,3 +207,35 @@ def test_every_registry_variant_with_outlier_rows(tg, tag):
     yi = tg.run_variant(tag, Xi, W, bi, cfg).values
     yg = tg.run_variant(tag, Xi, W, bi, tg.GemmConfig(method="gather", alpha=alpha, b=512)).values
     assert np.array_equal(yi, yg), tag
+
+
+def test_outlier_rows_without_an_exact_format(tg):
+    """tg_gemm_tiles with exact == NULL (no reference-order format to walk): shed rows still get
+    their listed terms, and a row whose rest is out of the epilogue's scale range keeps all
+    its entries in the limbs (the fp64 recombination then sees the whole row)."""
+    import ctypes
+
+    from paper_2510_06957_b200 import _native as nat
+
+    rng = np.random.default_rng(77)
+    M, K, N = 24, 1024, 128
+    W = _w(rng, K, N, 0.5)
+    X = rng.standard_normal((M, K)).astype(np.float32)
+    X[:, rng.choice(K, 4, replace=False)] *= np.float32(300.0)   # every row sheds four entries
+    X[7, :] *= np.float32(1e-33)                                 # the rest of row 7: scale 2^s with s > 100
+    X[7, 3] = np.float32(2e-20)
+    b = rng.standard_normal(N).astype(np.float32)
+    t = tg.tcsc_from_dense(torch.from_numpy(W).cuda())
+    tiles = t.tiles()
+    dX, db = torch.from_numpy(X).cuda(), torch.from_numpy(b).cuda()
+    y = torch.empty((M, N), dtype=torch.float32, device="cuda")
+    L = nat.load()
+    ws = torch.empty(L.tg_gemm_workspace_bytes(M, K, N), dtype=torch.uint8, device="cuda")
+    flags = torch.zeros(6, dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    P = lambda v: ctypes.c_void_p(v.data_ptr())
+    nat.call("tg_gemm_tiles", P(dX), M, K, K, P(tiles), N, P(db), P(y), N, 0, 0.0, None, P(ws), ws.numel(),
+             P(flags), st)
+    torch.cuda.synchronize()
+    nw, sc = _bars(y.cpu().numpy(), X, W, b)
+    assert nw <= TOL and sc <= TOL, (nw, sc)
