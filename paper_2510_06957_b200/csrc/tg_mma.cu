@@ -895,49 +895,55 @@ __device__ __forceinline__ void host_copy_tile(const MmaParams& p, const float* 
 
 // Outlier terms of 16 consecutive rows for this lane's column n: corr[r] = sum over row
 // (m_first + r)'s listed entries of W[k, n] * x, in list order (ascending k: a fixed order).
-// The whole warp cooperates, in two memory round trips:
-//   1. lane l loads entry l of each of the 16 lists (a list is 32 slots = 256 contiguous bytes;
-//      slots beyond a row's count hold stale pairs and are masked), with the 16 counts;
-//   2. lane l loads, for each of ITS 16 entries, the two words of the row-major 2-bit plane
-//      behind the tiles that hold W[k, .] for the warp's 32 columns (16 columns per word);
-// then entry i of every row is broadcast from lane i by shuffle (a rolled loop over i, the rows
-// unrolled) and each lane adds its column's term.  Branch-free: bit 1 of a code flips the sign
-// of x, bit 0 selects x or 0.  (One lane per column walking its rows' lists paid ~0.5 us of L2
-// latency per entry; a fully unrolled (entry, row) nest was 150 KB of code, fetch-bound.)
+// The whole warp cooperates, in two memory round trips per pass of 16 entries of every row:
+//   1. lanes l and l + 16 load entry 16 pass + l % 16 of each of the 16 lists (slots beyond a
+//      row's count hold stale pairs and are masked), with the 16 counts;
+//   2. each loads, for each of those entries, ITS half-warp's word of the row-major 2-bit plane
+//      behind the tiles (16 columns per word: W[k, .] for the warp's 32 columns is two words);
+// then entry i of every row is broadcast from lane i (to lanes 0-15) and lane i + 16 (to lanes
+// 16-31) by shuffle -- a rolled loop over i, the rows unrolled, two shuffles per (row, entry) --
+// and each lane adds its column's term.  Branch-free: bit 1 of a code flips the sign of x, bit
+// 0 selects x or 0.  (One lane per column walking its rows' lists paid ~0.5 us of L2 latency
+// per entry; a fully unrolled (entry, row) nest was 150 KB of code, fetch-bound.)
 __device__ __noinline__ void outlier_chunk(const MmaParams& p, int m_first, int n, float* corr) {
-  static_assert(kOutlierCap == 32, "one list slot per lane");
+  static_assert(kOutlierCap == 32, "two passes of 16 entries");
   const int lane = int(threadIdx.x) & 31;
-  const int hi = lane >> 4;
-  const int2* lst = p.olist + int64_t(m_first) * kOutlierCap + lane;
-  const uint2* wpair = reinterpret_cast<const uint2*>(p.wrows + ((n - lane) >> 4));  // (n - lane: a multiple of 32)
-  const int64_t kstride = p.N_pad >> 5;  // row pitch of the plane in word pairs
+  const int hi = lane >> 4, lo = lane & 15;
+  const uint32_t* wword = p.wrows + (n >> 4);  // this lane's word of a plane row (n >> 4 = warp base + hi)
+  const int64_t kstride = p.N_pad >> 4;        // row pitch of the plane in words
   const int sh = 2 * (n & 15);
-  const int cnt_l = __ldg(p.ocount + m_first + (lane & 15));  // lane j (and j + 16) holds row j's count
-  int2 e[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) e[j] = __ldg(lst + j * kOutlierCap);
+  const int cnt_l = __ldg(p.ocount + m_first + lo);  // lanes j and j + 16 hold row j's count
   int maxcnt = cnt_l;
   for (int o = 8; o; o >>= 1) maxcnt = max(maxcnt, __shfl_xor_sync(0xffffffffu, maxcnt, o));
-  uint2 wv[16];
-  float xv[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const bool live = lane < __shfl_sync(0xffffffffu, cnt_l, j);
-    xv[j] = live ? __int_as_float(e[j].y) : 0.f;  // (x = 0, codes 0: adds 0)
-    wv[j] = live ? __ldg(wpair + int64_t(e[j].x) * kstride) : make_uint2(0u, 0u);
-  }
   float acc[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) acc[j] = 0.f;
 #pragma unroll 1
-  for (int i = 0; i < maxcnt; ++i) {
+  for (int pass = 0; 16 * pass < maxcnt; ++pass) {
+    const int ei = 16 * pass + lo;  // the entry this lane holds, of every row
+    const int2* lst = p.olist + int64_t(m_first) * kOutlierCap + ei;
+    int2 e[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) e[j] = __ldg(lst + j * kOutlierCap);
+    uint32_t wv[16];
+    float xv[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const float x = __shfl_sync(0xffffffffu, xv[j], i);
-      const uint32_t w0 = __shfl_sync(0xffffffffu, wv[j].x, i), w1 = __shfl_sync(0xffffffffu, wv[j].y, i);
-      const uint32_t code = (hi ? w1 : w0) >> sh;
-      const float xs = __int_as_float(__float_as_int(x) ^ int((code & 2u) << 30));
-      acc[j] += (code & 1u) ? xs : 0.f;
+      const bool live = ei < __shfl_sync(0xffffffffu, cnt_l, j);
+      xv[j] = live ? __int_as_float(e[j].y) : 0.f;  // (x = 0, codes 0: adds 0)
+      wv[j] = live ? __ldg(wword + int64_t(e[j].x) * kstride) : 0u;
+    }
+    const int iend = min(16, maxcnt - 16 * pass);
+#pragma unroll 1
+    for (int i = 0; i < iend; ++i) {
+      const int src = i + 16 * hi;  // the lane of my half-warp that holds entry i
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float x = __shfl_sync(0xffffffffu, xv[j], src);
+        const uint32_t code = __shfl_sync(0xffffffffu, wv[j], src) >> sh;
+        const float xs = __int_as_float(__float_as_int(x) ^ int((code & 2u) << 30));
+        acc[j] += (code & 1u) ? xs : 0.f;
+      }
     }
   }
 #pragma unroll
