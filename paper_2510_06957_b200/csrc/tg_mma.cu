@@ -1348,6 +1348,15 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
         tmem_ld16(tbase + 2 * MT + mm, r2);
         tmem_ld_wait();
 #endif
+        // The accumulator goes back to the MMA warp as soon as this warp's LAST chunk is in
+        // registers, before that chunk is emitted (with a single accumulator, MT = 80, the MMAs
+        // of the next unit wait for this; with two it only matters when the epilogue is the
+        // slower side).
+        if (mm + MSTEP >= MT) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
         if (et == 0 && lu == 0) TG_STAMP(7, 220 + mm / 16);
         if (p.splits == 1) {
           emit16_limbs<COMPACT>(r0, r1, r2, ctx(mm), p, npos, any_bad);
@@ -1365,10 +1374,6 @@ __global__ void __launch_bounds__(MmaCfg<MT>::THREADS, 1)
           }
         }
       }
-      // TMEM buffer can be reused by the MMA warp
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
       if (et == 0 && lu == 0) TG_STAMP(7, 120);
 
       if (p.splits > 1 && !ghost) {
