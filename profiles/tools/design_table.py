@@ -1,7 +1,8 @@
 #!/usr/bin/env python
-"""Markdown tables of DESIGN.md section 5 from a capture directory's bench lines.
+"""Markdown tables of DESIGN.md section 5 from a capture directory's bench lines and timelines.
 
-    python profiles/tools/design_table.py profiles/r02_v3
+    python profiles/tools/design_table.py profiles/r02_v3            # print
+    python profiles/tools/design_table.py profiles/r02_v3 --write    # and replace them in DESIGN.md
 """
 from __future__ import annotations
 
@@ -18,8 +19,59 @@ def line(d: str, name: str):
     return json.loads(txt[-1]) if txt else None
 
 
+def timelines(d: str) -> str:
+    """The milestone table of the four step timelines (profiles/tools/gtrace.py output)."""
+    def col(name):
+        out = {}
+        for l in open(os.path.join(d, name)).read().splitlines()[1:]:
+            pr = l.split()
+            if "last" not in pr:
+                continue
+            j = len(pr) - 1 - pr[::-1].index("last")
+            out[" ".join(pr[1:j - 2])] = (pr[j - 1], pr[j + 1])
+        return out
+
+    cols = [col(f) for f in ("timeline_cfg4.txt", "timeline_cfg4_outliers_8x100.txt", "timeline_cfg2.txt",
+                             "timeline_cfg2_outliers_8x100.txt")]
+    names = [("split CTA start", "X split: CTA start"), ("split row done", "X split: row done"),
+             ("GEMM CTA start", "GEMM CTA resident (programmatic launch)"),
+             ("dep wait returned", "`griddepcontrol.wait` returns"), ("first MMA commit", "first MMA stage committed"),
+             ("outlier terms: start", "epilogue: outlier lookups start (first unit)"),
+             ("outlier terms: done", "epilogue: outlier lookups done"), ("last MMA issued", "last MMA issued"),
+             ("accumulator ready", "accumulator ready"), ("epilogue done", "epilogue done"), ("CTA exit", "CTA exit")]
+    rows = ["| milestone (first – last CTA) | cfg4 | cfg4, 8 channels at 100× | cfg2 | cfg2, 8 channels at 100× |",
+            "|---|---|---|---|---|"]
+    for k, label in names:
+        rows.append(f"| {label} | " + " | ".join(f"{c[k][0]} – {c[k][1]}" for c in cols) + " |")
+    return "\n".join(rows)
+
+
+def write_design(d: str, tables: str) -> None:
+    """Replace the bench tables and the timeline table of DESIGN.md section 5."""
+    root = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    path = os.path.join(root, "DESIGN.md")
+    s = open(path).read()
+    a, b = s.index("| config | step | split / GEMM |"), s.index("(`cfg1` is launch-bound;")
+    s = s[:a] + tables + "\n\n" + s[b:]
+    a, b = s.index("| milestone (first – last CTA) |"), s.index("cfg4 spends ")
+    s = s[:a] + timelines(d) + "\n\n" + s[b:]
+    open(path, "w").write(s)
+
+
 def main() -> None:
     d = sys.argv[1]
+    if "--write" in sys.argv:
+        import contextlib
+        import io
+
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            sys.argv.remove("--write")
+            main()
+        parts = buf.getvalue().strip().split("\n\n")
+        write_design(d, parts[0] + "\n\n" + parts[1])
+        print(buf.getvalue())
+        return
     rows = [("cfg1 64×512×512", "bench_cfg1.json"), ("cfg2 256×4096×4096 +PReLU", "bench_cfg2.json"),
             ("cfg3 512×8192² s=1/16", "bench_cfg3_s1_16.json"), ("cfg3 s=1/8", "bench_cfg3_s1_8.json"),
             ("cfg3 s=1/4", "bench_cfg3_s1_4.json"), ("cfg3 s=1/2", "bench_cfg3_s1_2.json"),
