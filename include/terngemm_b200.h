@@ -214,7 +214,7 @@ typedef struct {
  *     the limbs with exact int32 accumulation in TMEM; the epilogue recombines the
  *     limbs exactly, scales in fp64, adds the bias, rounds once to fp32 and
  *     applies PReLU.  Rows whose nonzero entries span more than a 16x
- *     max/rms dynamic range first shed their few large entries (at most 32 per
+ *     max/rms dynamic range first shed their few large entries (at most 128 per
  *     row, e.g. LLM outlier channels): prepare lists them as (k, x) pairs, the limbs
  *     carry the rest at the rest's own scale, and the epilogue adds the listed
  *     terms from the packed tile words in fp32.  Rows that stay wide after that

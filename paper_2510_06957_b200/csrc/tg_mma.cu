@@ -114,7 +114,7 @@ __device__ __forceinline__ void zero_split_counters(double* rscale, int64_t M_pa
 // the limbs carry the rest at the rest's own scale, and the GEMM epilogue adds sum_k (+-x) of
 // the listed entries, W[k, n] read from the row-major 2-bit plane behind the tiles (exact fp32
 // adds, a fixed order).  Rows that stay wide after kOutlierRounds rounds keep the exact walk.
-constexpr int kOutlierCap = 32;
+constexpr int kOutlierCap = 128;  // (1 KB of list per row)
 constexpr float kOutlierCut = 8.f;
 constexpr int kOutlierRounds = 4;
 // Tail of the prepare workspace, relative to the row scales: split-K counters, the per-row
@@ -906,7 +906,7 @@ __device__ __forceinline__ void host_copy_tile(const MmaParams& p, const float* 
 // 0 selects x or 0.  (One lane per column walking its rows' lists paid ~0.5 us of L2 latency
 // per entry; a fully unrolled (entry, row) nest was 150 KB of code, fetch-bound.)
 __device__ __noinline__ void outlier_chunk(const MmaParams& p, int m_first, int n, float* corr) {
-  static_assert(kOutlierCap == 32, "two passes of 16 entries");
+  static_assert(kOutlierCap % 16 == 0, "passes of 16 entries");
   const int lane = int(threadIdx.x) & 31;
   const int hi = lane >> 4, lo = lane & 15;
   const uint32_t* wword = p.wrows + (n >> 4);  // this lane's word of a plane row (n >> 4 = warp base + hi)

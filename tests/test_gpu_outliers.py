@@ -73,7 +73,7 @@ def test_outlier_channels_stay_on_tensor_cores(tg, M, K, N, scale, nch):
     t = tg.interleaved_blocked_from_dense(W)
     st = _stats(tg, X, t, b)
     assert st["exact_rows"] == 0, st
-    assert st["outlier_rows"] == M and 0 < st["outlier_entries"] <= 32 * M, st
+    assert st["outlier_rows"] == M and 0 < st["outlier_entries"] <= 128 * M, st
     for alpha in (None, 0.25):
         y = _gemm(tg, X, W, b, alpha).values
         nw, sc = _bars(y, X, W, b, alpha)
@@ -112,7 +112,7 @@ def test_rows_that_cannot_shed_keep_the_exact_walk(tg):
     M, K, N = 20, 2048, 96
     W = _w(rng, K, N, 0.5)
     X = rng.standard_normal((M, K)).astype(np.float32)
-    X[2, rng.choice(K, 40, replace=False)] *= np.float32(1000.0)  # 40 > kOutlierCap
+    X[2, rng.choice(K, 400, replace=False)] *= np.float32(1000.0)  # more than the list's 128 entries
     X[5, :] *= np.float32(1e-30)
     X[5, 9] = 3e-20  # the rest's scale 2^s has s > 100
     X[9, 100] = 7e5  # one entry: shed
@@ -183,13 +183,14 @@ def test_heavy_tailed_rows_fuzz(tg, seed):
                                  "horizontal", "vectorized_optimal"])
 def test_every_registry_variant_with_outlier_rows(tg, tag):
     """Every registry tag (kernels/__init__.py:98-198) on the tensor-core path with outlier
-    channels, a row that cannot shed (exact walk of that variant's own order) and a plain row."""
+    channels, a row that cannot shed (exact walk of that variant's own order) and plain rows."""
     rng = np.random.default_rng(sum(map(ord, tag)))
     M, K, N = 37, 1300, 96
     W = _w(rng, K, N)
     X = rng.standard_normal((M, K)).astype(np.float32)
     X[:30, rng.choice(K, 5, replace=False)] *= np.float32(200.0)      # rows 0-29: five outlier channels
-    X[31, rng.choice(K, 50, replace=False)] *= np.float32(500.0)      # row 31: more entries than the list holds
+    X[31, :] *= np.float32(1e-33)                                      # row 31 cannot shed: the rest's scale
+    X[31, 7] = np.float32(3e-20)                                       # is outside the epilogue's range
     b = rng.standard_normal(N).astype(np.float32)
     spec = tg.get_variant(tag)
     alpha = 0.25 if spec.supports_alpha else None
